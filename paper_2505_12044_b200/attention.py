@@ -1,0 +1,445 @@
+"""Attention with additive bias on B200 — drop-in for pkg/src/flashbias/attention.py.
+
+Public names and argument meaning follow the reference:
+
+* ``flashbias_attention(q, k, v, fq, fk, mask="none", tiles=None)``
+  (attention.py:205-230): logits = q k^T / sqrt(C) + fq fk^T with C the
+  ORIGINAL channel count; computed as the widened contraction
+  [q | sqrt(C) fq][k | fk]^T / sqrt(C) inside the tcgen05 kernel (K1).
+* ``tiled_attention(q, k, v, bias=NO_BIAS, mask, tiles, scale)``
+  (attention.py:140-202): NoBias / DenseBias (K3, bias tile streamed by TMA) /
+  FactoredBias (K1 with premultiplier 1/scale so the factor term is unscaled).
+* ``reference_attention`` / ``attention_weights`` (attention.py:111-137): the
+  materialised formula, evaluated on the GPU with torch (validation helper).
+* ``TileConfig`` / ``choose_tile_sizes`` (attention.py:38-74): kept for API
+  compatibility; on B200 the tile is fixed by UMMA (128 x 128), ``tiles`` is
+  validated and otherwise advisory (outputs are tiling-invariant,
+  tests/test_attention.py:143-158 of the reference).
+
+Inputs: numpy arrays (reference style, 2-D per head, returned as float64
+numpy) or torch tensors ([N, C], [H, N, C] or [B, H, N, C]) on CPU or CUDA.
+Compute precision follows the input: bf16/fp16 -> tcgen05 kernels (forward and
+backward, autograd-enabled); fp32/fp64 -> the fp32 SIMT kernel (forward).
+Host inputs are copied to the GPU and results copied back (the e2e path).
+There is no CPU fallback: without the CUDA library every call raises.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .bias import NO_BIAS, DenseBias, FactoredBias, NoBias, _is_torch
+from .errors import ConfigError, MaskError, ShapeError, ValidationError
+
+MASK_NONE = "none"
+MASK_CAUSAL = "causal"
+MASK_FILL = float(np.finfo(np.float64).min)
+_SUPPORTED_D = (32, 64, 128)
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Rows per query block and per key/value block (advisory on B200)."""
+
+    b_q: int
+    b_kv: int
+    sram_budget_bytes: Optional[int] = None
+
+    def __post_init__(self):
+        if self.b_q < 1 or self.b_kv < 1:
+            raise ConfigError("tile sizes must be >= 1")
+
+
+def choose_tile_sizes(c: int, r: int, sram_bytes: int, dtype_bytes: int) -> TileConfig:
+    """Reference sizing rule b_q = floor(S / (4 e (c+r))), b_kv = min(b_q, c+r),
+    rounded down to multiples of 8 (attention.py:51-74)."""
+    width = c + r
+    if width < 1:
+        raise ConfigError("c + r must be >= 1")
+    need = 4 * dtype_bytes * width
+    if sram_bytes < need:
+        raise ConfigError(f"sram_bytes={sram_bytes} below minimum {need} for width c+r={width}")
+    b_q = sram_bytes // need
+    b_kv = min(b_q, width)
+    r8 = lambda x: x - x % 8 if x >= 8 else x  # noqa: E731
+    return TileConfig(max(1, r8(b_q)), max(1, r8(b_kv)), sram_bytes)
+
+
+# ---------------------------------------------------------------- input plumbing
+class _Shape:
+    """Remember how a user input was laid out so the result mirrors it."""
+
+    def __init__(self, x):
+        self.numpy = not _is_torch(x)
+        self.device = None if self.numpy else x.device
+        self.dtype = None if self.numpy else x.dtype
+        self.ndim = np.ndim(x) if self.numpy else x.dim()
+
+
+def _to_torch(x, name: str, device, dtype=None):
+    import torch
+    if _is_torch(x):
+        t = x
+        if t.dim() < 2 or t.dim() > 4:
+            raise ShapeError(f"{name} must be 2-D, 3-D or 4-D, got ndim={t.dim()}")
+    else:
+        a = np.asarray(x, dtype=np.float64)
+        if a.ndim != 2:
+            raise ShapeError(f"{name} must be 2-D, got ndim={a.ndim}")
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None and t.dtype != dtype:
+        t = t.to(dtype)
+    if t.device != device:
+        t = t.to(device, non_blocking=True)
+    while t.dim() < 4:
+        t = t.unsqueeze(0)
+    return t
+
+
+def _compute_dtype(shape: _Shape, precision: Optional[str]):
+    import torch
+    if precision is not None:
+        return {"bf16": torch.bfloat16, "fp16": torch.float16, "fp32": torch.float32}[precision]
+    if shape.numpy or shape.dtype in (torch.float64, torch.float32):
+        return torch.float32
+    if shape.dtype in (torch.bfloat16, torch.float16):
+        return shape.dtype
+    raise ValidationError(f"unsupported dtype {shape.dtype}")
+
+
+def _validate_mask(mask: str, n: int, m: int) -> None:
+    if mask not in (MASK_NONE, MASK_CAUSAL):
+        raise ValidationError(f"unknown mask {mask!r}")
+    if mask == MASK_CAUSAL and n != m:
+        raise MaskError(f"causal mask requires N == M, got {n} x {m}")
+
+
+def _validate_qkv_shapes(q, k, v) -> None:
+    if q.shape[-1] != k.shape[-1]:
+        raise ShapeError(f"q and k channel counts differ: {q.shape[-1]} vs {k.shape[-1]}")
+    if k.shape[-2] != v.shape[-2]:
+        raise ShapeError(f"k and v row counts differ: {k.shape[-2]} vs {v.shape[-2]}")
+
+
+def _pad_last(t, to: int):
+    import torch
+    if t.shape[-1] == to:
+        return t.contiguous()
+    out = torch.zeros(*t.shape[:-1], to, dtype=t.dtype, device=t.device)
+    out[..., : t.shape[-1]] = t
+    return out
+
+
+def _padded_head_dim(c: int) -> int:
+    for d in _SUPPORTED_D:
+        if c <= d:
+            return d
+    raise ConfigError(f"head dim {c} > 128 is not supported by the sm_100a kernels")
+
+
+def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int = 64) -> int:
+    """bf16 k-way split level for logical fp32 factors.
+
+    1 when both factors are exactly representable in bf16; otherwise the
+    smallest k whose error bound sum_r |a_r|max |b_r|max * k * 2^(-8k-1) is
+    below ``tol`` (logit units), limited by R * k(k+1)/2 <= max_cols.
+    """
+    import torch
+    a = fq.float() * premul
+    b = fk.float()
+    if torch.equal(a.to(torch.bfloat16).float(), a) and torch.equal(b.to(torch.bfloat16).float(), b):
+        return 1
+    r = a.shape[-1]
+    amax = a.abs().amax(dim=tuple(range(a.dim() - 1)))
+    bmax = b.abs().amax(dim=tuple(range(b.dim() - 1)))
+    scale = float((amax * bmax).sum())
+    best = 1
+    for k in (1, 2, 3):
+        if r * k * (k + 1) // 2 > max_cols:
+            break
+        best = k
+        if scale * k * 2.0 ** (-8 * k - 1) <= tol:
+            return k
+    return best
+
+
+def prepare_factor_panels(fq, fk, premul: float, split: int, dtype):
+    """Device-ready panels (fb_prepare_factors): uq = split(premul*fq), uk = split(fk)."""
+    import torch
+    lib = _lib.lib()
+    fq32 = fq.float().contiguous()
+    fk32 = fk.float().contiguous()
+    r = fq32.shape[-1]
+    rpad = int(lib.fb_factor_rpad(r, split))
+    uq = torch.empty(*fq32.shape[:-1], rpad, dtype=dtype, device=fq32.device)
+    uk = torch.empty(*fk32.shape[:-1], rpad, dtype=dtype, device=fk32.device)
+    s = _lib.stream_ptr(fq32.device)
+    _lib.check(lib.fb_prepare_factors(_lib.ref(_lib.desc(fq32)), 0, split, float(premul), _lib.ref(_lib.desc(uq)), s))
+    _lib.check(lib.fb_prepare_factors(_lib.ref(_lib.desc(fk32)), 1, split, 1.0, _lib.ref(_lib.desc(uk)), s))
+    return uq, uk
+
+
+def fold_factor_grads(dpanel, like, side: int, split: int, postmul: float):
+    """fb_fold_factor_grads: split-panel gradients -> logical factor gradient shaped like ``like``."""
+    import torch
+    lib = _lib.lib()
+    out = torch.empty(like.shape, dtype=torch.float32, device=dpanel.device)
+    _lib.check(lib.fb_fold_factor_grads(_lib.ref(_lib.desc(dpanel)), side, split, float(postmul),
+                                        _lib.ref(_lib.desc(out)), _lib.stream_ptr(dpanel.device)))
+    return out
+
+
+# ---------------------------------------------------------------- core launches
+def _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale, need_lse=True):
+    import torch
+    lib = _lib.lib()
+    B, H, N, _ = q.shape
+    o = torch.empty(B, H, N, v.shape[-1], dtype=q.dtype, device=q.device)
+    lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device) if need_lse else None
+    D = _lib.desc
+    _lib.check(lib.fb_attn_fwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
+                               _lib.ref(D(bias)), mask_code, float(scale), _lib.ref(D(o)), _lib.ref(D(lse)),
+                               _lib.stream_ptr(q.device)))
+    return o, lse
+
+
+def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad):
+    import torch
+    lib = _lib.lib()
+    D = _lib.desc
+    dq = torch.empty_like(q)
+    dk = torch.empty_like(k)
+    dv = torch.empty_like(v)
+    duq = duk = None
+    if want_fgrad and uq is not None:
+        B, H = q.shape[0], q.shape[1]
+        duq = torch.empty(B, H, q.shape[2], uq.shape[-1], dtype=torch.float32, device=q.device)
+        duk = torch.empty(B, H, k.shape[2], uk.shape[-1], dtype=torch.float32, device=q.device)
+    dq_d, k_d = D(q), D(k)
+    ws_bytes = int(lib.fb_bwd_workspace_bytes(_lib.ref(dq_d), _lib.ref(k_d)))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+    _lib.check(lib.fb_attn_bwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
+                               _lib.ref(D(bias)), _lib.ref(D(o)), _lib.ref(D(lse)), _lib.ref(D(do)), mask_code,
+                               float(scale), _lib.ref(D(dq)), _lib.ref(D(dk)), _lib.ref(D(dv)), _lib.ref(D(duq)),
+                               _lib.ref(D(duk)), ws.data_ptr(), ws_bytes, _lib.stream_ptr(q.device)))
+    return dq, dk, dv, duq, duk
+
+
+def _make_fn():
+    import torch
+
+    class FlashBiasFunction(torch.autograd.Function):
+        """Autograd wrapper: forward K1/K3, backward K2/K4 (+ factor gradients)."""
+
+        @staticmethod
+        def forward(ctx, q, k, v, fq, fk, bias, mask_code, scale, premul, split):
+            uq = uk = None
+            if fq is not None:
+                uq, uk = prepare_factor_panels(fq, fk, premul, split, q.dtype)
+            o, lse = _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale)
+            ctx.save_for_backward(q, k, v, uq, uk, bias, o, lse, fq, fk)
+            ctx.cfg = (mask_code, scale, premul, split)
+            return o
+
+        @staticmethod
+        def backward(ctx, do):
+            q, k, v, uq, uk, bias, o, lse, fq, fk = ctx.saved_tensors
+            mask_code, scale, premul, split = ctx.cfg
+            if bias is not None and ctx.needs_input_grad[5]:
+                raise NotImplementedError("gradient w.r.t. a dense bias is not produced (static bias)")
+            want_fg = fq is not None and (ctx.needs_input_grad[3] or ctx.needs_input_grad[4])
+            dq, dk, dv, duq, duk = _bwd_launch(q, k, v, uq, uk, bias, o, lse, do.contiguous(), mask_code, scale,
+                                               want_fg)
+            dfq = dfk = None
+            if want_fg:
+                dfq = fold_factor_grads(duq, fq, 0, split, premul).to(fq.dtype)
+                dfk = fold_factor_grads(duk, fk, 1, split, 1.0).to(fk.dtype)
+            return dq, dk, dv, dfq, dfk, None, None, None, None, None
+
+    return FlashBiasFunction
+
+
+_FN = None
+
+
+def _fn():
+    global _FN
+    if _FN is None:
+        _FN = _make_fn()
+    return _FN
+
+
+def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none", scale=None,
+               precision=None, split=None):
+    """Shared driver: normalise inputs, run the kernel, mirror the input layout."""
+    import torch
+    shp = _Shape(q)
+    _validate_qkv_shapes(q, k, v)
+    n, m, c = int(q.shape[-2]), int(k.shape[-2]), int(q.shape[-1])
+    _validate_mask(mask, n, m)
+    if scale is None:
+        scale = 1.0 / math.sqrt(c)
+    if not torch.cuda.is_available():
+        raise RuntimeError("flashbias: CUDA device required (no CPU fallback)")
+    device = shp.device if (shp.device is not None and shp.device.type == "cuda") else torch.device("cuda")
+    cdt = _compute_dtype(shp, precision)
+    qt = _to_torch(q, "q", device, cdt)
+    kt = _to_torch(k, "k", device, cdt)
+    vt = _to_torch(v, "v", device, cdt)
+    if qt.shape[:2] != kt.shape[:2] or kt.shape[:2] != vt.shape[:2]:
+        raise ShapeError("batch/head extents of q, k, v differ")
+    fqt = fkt = None
+    if fq is not None:
+        fqt = _to_torch(fq, "fq", device)
+        fkt = _to_torch(fk, "fk", device)
+        if fqt.shape[-1] != fkt.shape[-1]:
+            raise ShapeError(f"factor ranks differ: {fqt.shape[-1]} vs {fkt.shape[-1]}")
+        if fqt.shape[-2] != n:
+            raise ShapeError(f"fq rows {fqt.shape[-2]} do not match q rows {n}")
+        if fkt.shape[-2] != m:
+            raise ShapeError(f"fk rows {fkt.shape[-2]} do not match k rows {m}")
+    bt = None
+    if bias is not None:
+        bt = _to_torch(bias, "bias", device)
+        if tuple(bt.shape[-2:]) != (n, m):
+            raise ShapeError(f"bias shape {tuple(bt.shape[-2:])} does not match logits {(n, m)}")
+    mask_code = _lib.MASK_CODES[mask]
+
+    if cdt == torch.float32:
+        qf, kf, vf = (t.contiguous() for t in (qt, kt, vt))
+        uq = uk = None
+        if fqt is not None:
+            uq = (fqt.float() * premul).contiguous()
+            uk = fkt.float().contiguous()
+        bf = bt.float().contiguous() if bt is not None else None
+        o, _ = _fwd_launch(qf, kf, vf, uq, uk, bf, mask_code, scale, need_lse=False)
+    else:
+        dp = _padded_head_dim(max(c, int(vt.shape[-1])))
+        qp, kp, vp = _pad_last(qt, dp), _pad_last(kt, dp), _pad_last(vt, dp)
+        bp = None
+        if bt is not None:
+            bt = bt.to(cdt)
+            if m % 8:
+                store = torch.zeros(*bt.shape[:-1], (m + 7) // 8 * 8, dtype=cdt, device=device)
+                store[..., :m] = bt
+                bp = store[..., :m]
+            else:
+                bp = bt.contiguous()
+        sp = None
+        if fqt is not None:
+            sp = split or choose_split(fqt, fkt, premul)
+        o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(scale), float(premul), sp)
+        o = o[..., : vt.shape[-1]]
+    return _mirror(o, shp)
+
+
+def _mirror(o, shp: _Shape):
+    if shp.numpy:
+        return o.reshape(o.shape[-2], o.shape[-1]).double().cpu().numpy()
+    while o.dim() > shp.ndim:
+        o = o.squeeze(0)
+    if shp.device is not None and o.device != shp.device:
+        o = o.to(shp.device)
+    if o.dtype != shp.dtype:
+        o = o.to(shp.dtype)
+    return o
+
+
+def _check_tiles(tiles) -> None:
+    if tiles is not None and not isinstance(tiles, TileConfig):
+        raise ValidationError("tiles must be a TileConfig")
+
+
+# ---------------------------------------------------------------- public API
+def flashbias_attention(q, k, v, fq, fk, mask: str = MASK_NONE, tiles: Optional[TileConfig] = None, *,
+                        precision: Optional[str] = None, split: Optional[int] = None):
+    """softmax(q k^T / sqrt(C) + fq fk^T) v without materialising the bias
+    (attention.py:205-230): widened contraction [q | sqrt(C) fq][k | fk]^T with
+    the original 1/sqrt(C) scale, folded into the tcgen05 kernel."""
+    _check_tiles(tiles)
+    c = int(q.shape[-1])
+    root_c = math.sqrt(c)
+    return _attention(q, k, v, fq=fq, fk=fk, premul=root_c, mask=mask, scale=1.0 / root_c,
+                      precision=precision, split=split)
+
+
+def tiled_attention(q, k, v, bias=NO_BIAS, mask: str = MASK_NONE, tiles: Optional[TileConfig] = None,
+                    scale: Optional[float] = None, *, precision: Optional[str] = None,
+                    split: Optional[int] = None):
+    """Streaming attention with NoBias / DenseBias / FactoredBias (attention.py:140-202)."""
+    _check_tiles(tiles)
+    c = int(q.shape[-1])
+    if scale is None:
+        scale = 1.0 / math.sqrt(c)
+    if isinstance(bias, NoBias):
+        return _attention(q, k, v, mask=mask, scale=scale, precision=precision)
+    if isinstance(bias, DenseBias):
+        return _attention(q, k, v, bias=bias.b, mask=mask, scale=scale, precision=precision)
+    if isinstance(bias, FactoredBias):
+        # the factor term is added unscaled: uq = fq / scale so scale*uq.uk = fq.fk
+        return _attention(q, k, v, fq=bias.fq, fk=bias.fk, premul=1.0 / scale, mask=mask, scale=scale,
+                          precision=precision, split=split)
+    raise ValidationError(f"unknown bias provider {type(bias).__name__}")
+
+
+def _dense_of(bias, n: int, m: int):
+    if isinstance(bias, NoBias):
+        return None
+    if isinstance(bias, DenseBias):
+        b = bias.b
+    elif isinstance(bias, FactoredBias):
+        b = bias.dense()
+    else:
+        raise ValidationError(f"unknown bias provider {type(bias).__name__}")
+    if tuple(b.shape[-2:]) != (n, m):
+        raise ShapeError(f"bias shape {tuple(b.shape[-2:])} does not match logits {(n, m)}")
+    return b
+
+
+def attention_weights(q, k, bias=NO_BIAS, mask: str = MASK_NONE, scale: Optional[float] = None):
+    """Row-stochastic weights of the materialised formula (attention.py:111-128), on the GPU in fp64."""
+    import torch
+    shp = _Shape(q)
+    if q.shape[-1] != k.shape[-1]:
+        raise ShapeError(f"q and k channel counts differ: {q.shape[-1]} vs {k.shape[-1]}")
+    n, m = int(q.shape[-2]), int(k.shape[-2])
+    _validate_mask(mask, n, m)
+    if scale is None:
+        scale = 1.0 / math.sqrt(q.shape[-1])
+    dev = torch.device("cuda")
+    qt = _to_torch(q, "q", dev, torch.float64)
+    kt = _to_torch(k, "k", dev, torch.float64)
+    logits = (qt @ kt.transpose(-1, -2)) * scale
+    b = _dense_of(bias, n, m)
+    if b is not None:
+        logits = logits + _to_torch(b, "bias", dev, torch.float64)
+    if mask == MASK_CAUSAL:
+        upper = torch.ones(n, m, dtype=torch.bool, device=dev).triu(1)
+        logits = logits.masked_fill(upper, MASK_FILL)
+    w = torch.softmax(logits, dim=-1)
+    return _mirror_f64(w, shp)
+
+
+def reference_attention(q, k, v, bias=NO_BIAS, mask: str = MASK_NONE, scale: Optional[float] = None):
+    """softmax(q k^T scale + bias + mask) v with the full logit matrix (attention.py:131-137)."""
+    import torch
+    _validate_qkv_shapes(q, k, v)
+    shp = _Shape(q)
+    w = attention_weights(q if not shp.numpy else np.asarray(q, dtype=np.float64), k, bias, mask, scale)
+    wt = w if _is_torch(w) else torch.from_numpy(w).cuda()
+    vt = _to_torch(v, "v", wt.device, torch.float64)
+    out = wt.to(torch.float64) @ vt
+    return _mirror_f64(out, shp)
+
+
+def _mirror_f64(t, shp: _Shape):
+    if shp.numpy:
+        return t.reshape(t.shape[-2], t.shape[-1]).cpu().numpy()
+    while t.dim() > shp.ndim:
+        t = t.squeeze(0)
+    return t

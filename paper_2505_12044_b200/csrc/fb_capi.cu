@@ -1,0 +1,432 @@
+// fb_capi.cu — the extern "C" boundary (include/flashbias_b200.h).
+//
+// Validation mirrors the reference's pre-compute checks
+// (pkg/src/flashbias/attention.py:77-93 _validate_qkv/_validate_mask and
+// 215-223 factor rank/row checks) and maps them onto status codes that the
+// Python shim turns back into ShapeError / MaskError / ConfigError /
+// ValidationError (errors.py:4-17).  No allocation, stream ordered.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/flashbias_b200.h"
+#include "fb_kernels.h"
+
+namespace fb {
+
+static thread_local char g_err[512] = "";
+static thread_local int64_t g_launches = 0;
+
+void note_launch(int n) { g_launches += n; }
+
+static int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FB_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+static size_t dtype_size(int dt) {
+  switch (dt) {
+    case FB_F32: return 4;
+    case FB_BF16: return 2;
+    case FB_F16: return 2;
+    case FB_F64: return 8;
+  }
+  return 0;
+}
+
+static Tensor4 to_t4(const fb_tensor* t) {
+  Tensor4 r;
+  r.data = t->data;
+  for (int i = 0; i < 4; ++i) {
+    r.shape[i] = t->shape[i];
+    r.stride[i] = t->shape[i] == 1 ? 0 : t->stride[i];
+  }
+  r.dtype = t->dtype;
+  return r;
+}
+
+// ------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// 4-D map over a [B,H,L,C] view with box [box_cols x 128 rows].
+static int make_map(CUtensorMap* map, const fb_tensor* t, int box_cols, int box_rows, int swizzle_bytes,
+                    const char* name) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(FB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const size_t es = dtype_size(t->dtype);
+  if (t->stride[3] != 1) return fail(FB_ESHAPE, "%s: last dim must be contiguous", name);
+  if (reinterpret_cast<uintptr_t>(t->data) % 16) return fail(FB_EVALUE, "%s: data must be 16-byte aligned", name);
+  cuuint64_t dims[4] = {(cuuint64_t)t->shape[3], (cuuint64_t)t->shape[2], (cuuint64_t)t->shape[1],
+                        (cuuint64_t)t->shape[0]};
+  cuuint64_t strides[3];
+  int64_t inner = t->shape[3] * (int64_t)es;
+  for (int i = 0; i < 3; ++i) {
+    const int dim = 2 - i;  // L, H, B
+    int64_t st = t->stride[dim] * (int64_t)es;
+    if (t->shape[dim] == 1 || t->stride[dim] == 0) st = inner;  // broadcast / unit dim
+    if (st % 16) return fail(FB_EVALUE, "%s: stride of dim %d (%lld bytes) not a multiple of 16", name, dim,
+                             (long long)st);
+    strides[i] = (cuuint64_t)st;
+    inner = st * (t->shape[dim] > 0 ? t->shape[dim] : 1);
+  }
+  cuuint32_t box[4] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUtensorMapDataType dt = t->dtype == FB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUresult r = enc(map, dt, 4, t->data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FB_ECUDA, "%s: cuTensorMapEncodeTiled failed (%d)", name, (int)r);
+  return FB_OK;
+}
+
+static inline int swz_for(int d) { return d * 2 >= 128 ? 128 : (d * 2 >= 64 ? 64 : 32); }
+
+// ------------------------------------------------------------ validation
+static int check_qkv(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v) {
+  if (!q || !k || !v) return fail(FB_EVALUE, "q, k, v are required");
+  for (int i = 0; i < 4; ++i)
+    if (q->shape[i] < 0 || k->shape[i] < 0 || v->shape[i] < 0) return fail(FB_ESHAPE, "negative extent");
+  if (q->shape[3] != k->shape[3])
+    return fail(FB_ESHAPE, "q and k channel counts differ: %lld vs %lld", (long long)q->shape[3],
+                (long long)k->shape[3]);
+  if (k->shape[2] != v->shape[2])
+    return fail(FB_ESHAPE, "k and v row counts differ: %lld vs %lld", (long long)k->shape[2],
+                (long long)v->shape[2]);
+  if (q->shape[0] != k->shape[0] || q->shape[1] != k->shape[1] || k->shape[0] != v->shape[0] ||
+      k->shape[1] != v->shape[1])
+    return fail(FB_ESHAPE, "batch/head extents of q, k, v differ");
+  if (q->dtype != k->dtype || k->dtype != v->dtype) return fail(FB_EVALUE, "q, k, v dtypes differ");
+  if (q->shape[2] < 1 || k->shape[2] < 1) return fail(FB_ESHAPE, "empty sequence");
+  return FB_OK;
+}
+
+static int check_mask(int mask, int64_t n, int64_t m) {
+  if (mask != FB_MASK_NONE && mask != FB_MASK_CAUSAL) return fail(FB_EVALUE, "unknown mask %d", mask);
+  if (mask == FB_MASK_CAUSAL && n != m)
+    return fail(FB_EMASK, "causal mask requires N == M, got %lld x %lld", (long long)n, (long long)m);
+  return FB_OK;
+}
+
+static bool bcast_ok(int64_t f, int64_t full) { return f == 1 || f == full; }
+
+static int check_factors(const fb_tensor* q, const fb_tensor* k, const fb_tensor* uq, const fb_tensor* uk) {
+  if ((uq == nullptr) != (uk == nullptr)) return fail(FB_EVALUE, "uq and uk must be given together");
+  if (!uq) return FB_OK;
+  if (uq->shape[3] != uk->shape[3])
+    return fail(FB_ESHAPE, "factor ranks differ: %lld vs %lld", (long long)uq->shape[3], (long long)uk->shape[3]);
+  if (uq->shape[2] != q->shape[2])
+    return fail(FB_ESHAPE, "fq rows %lld do not match q rows %lld", (long long)uq->shape[2], (long long)q->shape[2]);
+  if (uk->shape[2] != k->shape[2])
+    return fail(FB_ESHAPE, "fk rows %lld do not match k rows %lld", (long long)uk->shape[2], (long long)k->shape[2]);
+  if (!bcast_ok(uq->shape[0], q->shape[0]) || !bcast_ok(uq->shape[1], q->shape[1]) ||
+      !bcast_ok(uk->shape[0], q->shape[0]) || !bcast_ok(uk->shape[1], q->shape[1]))
+    return fail(FB_ESHAPE, "factor batch/head extents must be 1 or match q");
+  return FB_OK;
+}
+
+static int check_bias(const fb_tensor* q, const fb_tensor* k, const fb_tensor* bias) {
+  if (!bias) return FB_OK;
+  if (bias->shape[2] != q->shape[2] || bias->shape[3] != k->shape[2])
+    return fail(FB_ESHAPE, "bias shape (%lld, %lld) does not match logits (%lld, %lld)",
+                (long long)bias->shape[2], (long long)bias->shape[3], (long long)q->shape[2],
+                (long long)k->shape[2]);
+  if (!bcast_ok(bias->shape[0], q->shape[0]) || !bcast_ok(bias->shape[1], q->shape[1]))
+    return fail(FB_ESHAPE, "bias batch/head extents must be 1 or match q");
+  return FB_OK;
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+const char* fb_last_error(void) { return g_err; }
+int fb_abi_version(void) { return FB_ABI_VERSION; }
+int64_t fb_launch_count(int reset) {
+  const int64_t c = g_launches;
+  if (reset) g_launches = 0;
+  return c;
+}
+
+int64_t fb_factor_cols(int64_t rank, int split) { return rank * factor_pairs(split); }
+int64_t fb_factor_rpad(int64_t rank, int split) { return (fb_factor_cols(rank, split) + 15) / 16 * 16; }
+
+int fb_attn_fwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, const fb_tensor* uq,
+                const fb_tensor* uk, const fb_tensor* bias, int mask, float scale, fb_tensor* o,
+                fb_tensor* lse, void* stream) {
+  int rc;
+  if ((rc = check_qkv(q, k, v))) return rc;
+  if ((rc = check_mask(mask, q->shape[2], k->shape[2]))) return rc;
+  if ((rc = check_factors(q, k, uq, uk))) return rc;
+  if ((rc = check_bias(q, k, bias))) return rc;
+  if (!o) return fail(FB_EVALUE, "output tensor required");
+  if (o->shape[0] != q->shape[0] || o->shape[1] != q->shape[1] || o->shape[2] != q->shape[2] ||
+      o->shape[3] != v->shape[3])
+    return fail(FB_ESHAPE, "output shape mismatch");
+  if (o->dtype != q->dtype) return fail(FB_EVALUE, "output dtype must match q");
+  if (!(scale > 0.f) || !isfinite(scale)) return fail(FB_EVALUE, "scale must be positive and finite");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int B = (int)q->shape[0], H = (int)q->shape[1], N = (int)q->shape[2], M = (int)k->shape[2];
+  const int D = (int)q->shape[3];
+
+  if (q->dtype == FB_F32) {
+    if (D > 128 || v->shape[3] != D) return fail(FB_ECONFIG, "fp32 path supports D <= 128 with dv == d");
+    const int R = uq ? (int)uq->shape[3] : 0;
+    if (D + R > 320) return fail(FB_ECONFIG, "fp32 path supports D + R <= 320");
+    if ((uq && (uq->dtype != FB_F32 || uk->dtype != FB_F32)) || (bias && bias->dtype != FB_F32))
+      return fail(FB_EVALUE, "fp32 path needs fp32 factors and bias");
+    Tensor4 tq = to_t4(q), tk = to_t4(k), tv = to_t4(v), to = to_t4(o);
+    SimtParams p{};
+    p.B = B; p.H = H; p.N = N; p.M = M; p.D = D; p.R = R;
+    p.causal = mask == FB_MASK_CAUSAL;
+    p.scale = scale;
+    p.q = (const float*)q->data; p.q_sb = tq.stride[0]; p.q_sh = tq.stride[1]; p.q_sn = tq.stride[2];
+    p.k = (const float*)k->data; p.k_sb = tk.stride[0]; p.k_sh = tk.stride[1]; p.k_sn = tk.stride[2];
+    p.v = (const float*)v->data; p.v_sb = tv.stride[0]; p.v_sh = tv.stride[1]; p.v_sn = tv.stride[2];
+    if (uq) {
+      Tensor4 a = to_t4(uq), c = to_t4(uk);
+      p.uq = (const float*)uq->data; p.uq_sb = a.stride[0]; p.uq_sh = a.stride[1]; p.uq_sn = a.stride[2];
+      p.uk = (const float*)uk->data; p.uk_sb = c.stride[0]; p.uk_sh = c.stride[1]; p.uk_sn = c.stride[2];
+      if (uq->stride[3] != 1 || uk->stride[3] != 1) return fail(FB_ESHAPE, "factor last dim must be contiguous");
+    }
+    if (bias) {
+      Tensor4 a = to_t4(bias);
+      if (bias->stride[3] != 1) return fail(FB_ESHAPE, "bias last dim must be contiguous");
+      p.bias = (const float*)bias->data; p.bias_sb = a.stride[0]; p.bias_sh = a.stride[1]; p.bias_sn = a.stride[2];
+    }
+    for (const fb_tensor* t : {q, k, v, (const fb_tensor*)o})
+      if (t->stride[3] != 1) return fail(FB_ESHAPE, "last dim must be contiguous");
+    p.o = (float*)o->data; p.o_sb = to.stride[0]; p.o_sh = to.stride[1]; p.o_sn = to.stride[2];
+    p.lse = lse ? (float*)lse->data : nullptr;
+    cudaError_t e = launch_fwd_simt_f32(p, s);
+    return e == cudaSuccess ? FB_OK : cuda_fail(e, "fwd_simt_f32");
+  }
+
+  if (q->dtype != FB_BF16 && q->dtype != FB_F16) return fail(FB_EVALUE, "unsupported dtype %d", q->dtype);
+  if (D != 32 && D != 64 && D != 128)
+    return fail(FB_ECONFIG, "tcgen05 path supports head dim 32, 64, 128 (got %d); pad on the host", D);
+  if (v->shape[3] != D) return fail(FB_ECONFIG, "tcgen05 path needs dv == d");
+  int rp = 0;
+  if (uq) {
+    const int64_t rpad = uq->shape[3];
+    if (rpad % 16 || rpad > 64)
+      return fail(FB_ECONFIG, "factor panels must have Rpad in {16,32,48,64} (got %lld)", (long long)rpad);
+    if (uq->dtype != q->dtype || uk->dtype != q->dtype) return fail(FB_EVALUE, "factor panels must match q dtype");
+    rp = (int)(rpad / 16);
+  }
+  if (bias) {
+    if (uq) return fail(FB_ECONFIG, "tcgen05 path takes either factors or a dense bias, not both");
+    if (bias->dtype != q->dtype) return fail(FB_EVALUE, "dense bias dtype must match q");
+    if ((M * 2) % 16) return fail(FB_ECONFIG, "dense bias needs M to be a multiple of 8 (pad on the host)");
+  }
+  FwdMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  const int sw = swz_for(D);
+  if ((rc = make_map(&maps.q, q, sw / 2, 128, sw, "q"))) return rc;
+  if ((rc = make_map(&maps.k, k, sw / 2, 128, sw, "k"))) return rc;
+  if ((rc = make_map(&maps.v, v, sw / 2, 128, sw, "v"))) return rc;
+  if (uq) {
+    if ((rc = make_map(&maps.uq, uq, 16, 128, 32, "uq"))) return rc;
+    if ((rc = make_map(&maps.uk, uk, 16, 128, 32, "uk"))) return rc;
+  }
+  if (bias && (rc = make_map(&maps.bias, bias, 64, 128, 128, "bias"))) return rc;
+  if (o->stride[3] != 1 || (o->stride[2] * 2) % 16) return fail(FB_ESHAPE, "output rows must be contiguous, 16B aligned");
+  FwdParams p{};
+  p.B = B; p.H = H; p.N = N; p.M = M;
+  p.causal = mask == FB_MASK_CAUSAL;
+  p.num_pairs = (N + 255) / 256;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  Tensor4 to = to_t4(o);
+  p.o = o->data; p.o_sb = to.stride[0]; p.o_sh = to.stride[1]; p.o_sn = to.stride[2];
+  p.lse = lse ? (float*)lse->data : nullptr;
+  if (uq) {
+    p.uq_bb = uq->shape[0] == 1; p.uq_hb = uq->shape[1] == 1;
+    p.uk_bb = uk->shape[0] == 1; p.uk_hb = uk->shape[1] == 1;
+  }
+  if (bias) { p.bias_bb = bias->shape[0] == 1; p.bias_hb = bias->shape[1] == 1; }
+  cudaError_t e = launch_fwd_sm100(D, rp, bias != nullptr, q->dtype == FB_BF16, maps, p, s);
+  note_launch();
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "fwd_sm100");
+}
+
+size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k) {
+  (void)k;
+  if (!q) return 0;
+  return (size_t)q->shape[0] * q->shape[1] * q->shape[2] * sizeof(float) + 256;  // delta
+}
+
+int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, const fb_tensor* uq,
+                const fb_tensor* uk, const fb_tensor* bias, const fb_tensor* o, const fb_tensor* lse,
+                const fb_tensor* dout, int mask, float scale, fb_tensor* dq, fb_tensor* dk,
+                fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  int rc;
+  if ((rc = check_qkv(q, k, v))) return rc;
+  if ((rc = check_mask(mask, q->shape[2], k->shape[2]))) return rc;
+  if ((rc = check_factors(q, k, uq, uk))) return rc;
+  if ((rc = check_bias(q, k, bias))) return rc;
+  if (!o || !lse || !dout || !dq || !dk || !dv) return fail(FB_EVALUE, "o, lse, dout, dq, dk, dv are required");
+  if ((duq == nullptr) != (duk == nullptr)) return fail(FB_EVALUE, "duq and duk must be given together");
+  if (duq && !uq) return fail(FB_EVALUE, "factor gradients requested without factors");
+  if (q->dtype != FB_BF16 && q->dtype != FB_F16) return fail(FB_ECONFIG, "backward supports bf16/f16 only");
+  const int B = (int)q->shape[0], H = (int)q->shape[1], N = (int)q->shape[2], M = (int)k->shape[2];
+  const int D = (int)q->shape[3];
+  if (D != 32 && D != 64 && D != 128) return fail(FB_ECONFIG, "backward supports head dim 32, 64, 128");
+  if (workspace_bytes < fb_bwd_workspace_bytes(q, k) || !workspace) return fail(FB_ECONFIG, "workspace too small");
+  int rp = 0;
+  if (uq) {
+    const int64_t rpad = uq->shape[3];
+    if (rpad % 16 || rpad > 64) return fail(FB_ECONFIG, "factor panels must have Rpad in {16,32,48,64}");
+    rp = (int)(rpad / 16);
+  }
+  if (bias && uq) return fail(FB_ECONFIG, "either factors or a dense bias, not both");
+  if (bias && (M * 2) % 16) return fail(FB_ECONFIG, "dense bias needs M multiple of 8");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // preprocess delta = rowsum(dO * O)
+  float* delta = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+  Tensor4 tdelta{};
+  tdelta.data = delta;
+  tdelta.shape[0] = B; tdelta.shape[1] = H; tdelta.shape[2] = N; tdelta.shape[3] = 1;
+  tdelta.stride[0] = (int64_t)H * N; tdelta.stride[1] = N; tdelta.stride[2] = 1; tdelta.stride[3] = 1;
+  tdelta.dtype = FB_F32;
+  cudaError_t e = launch_bwd_preprocess(to_t4(o), to_t4(dout), tdelta, s);
+  if (e != cudaSuccess) return cuda_fail(e, "bwd_preprocess");
+
+  BwdMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  const int sw = swz_for(D);
+  if ((rc = make_map(&maps.q64, q, sw / 2, 64, sw, "q"))) return rc;
+  if ((rc = make_map(&maps.q128, q, sw / 2, 128, sw, "q"))) return rc;
+  if ((rc = make_map(&maps.do64, dout, sw / 2, 64, sw, "dout"))) return rc;
+  if ((rc = make_map(&maps.do128, dout, sw / 2, 128, sw, "dout"))) return rc;
+  if ((rc = make_map(&maps.k128, k, sw / 2, 128, sw, "k"))) return rc;
+  if ((rc = make_map(&maps.k64, k, sw / 2, 64, sw, "k"))) return rc;
+  if ((rc = make_map(&maps.v128, v, sw / 2, 128, sw, "v"))) return rc;
+  if ((rc = make_map(&maps.v64, v, sw / 2, 64, sw, "v"))) return rc;
+  if (uq) {
+    if ((rc = make_map(&maps.uq64, uq, 16, 64, 32, "uq"))) return rc;
+    if ((rc = make_map(&maps.uq128, uq, 16, 128, 32, "uq"))) return rc;
+    if ((rc = make_map(&maps.uk64, uk, 16, 64, 32, "uk"))) return rc;
+    if ((rc = make_map(&maps.uk128, uk, 16, 128, 32, "uk"))) return rc;
+  }
+  if (bias) {
+    if ((rc = make_map(&maps.biasT, bias, 64, 64, 128, "bias"))) return rc;
+    if ((rc = make_map(&maps.bias, bias, 64, 128, 128, "bias"))) return rc;
+  }
+  for (const fb_tensor* t : {(const fb_tensor*)dq, (const fb_tensor*)dk, (const fb_tensor*)dv})
+    if (t->stride[3] != 1 || (t->stride[2] * 2) % 16 || t->dtype != q->dtype || t->shape[3] != D)
+      return fail(FB_ESHAPE, "gradient outputs must match q dtype/shape with contiguous rows");
+  BwdParams p{};
+  p.B = B; p.H = H; p.N = N; p.M = M;
+  p.causal = mask == FB_MASK_CAUSAL;
+  p.scale = scale;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.lse = (const float*)lse->data;
+  p.delta = delta;
+  Tensor4 a;
+  a = to_t4(dq); p.dq = dq->data; p.dq_sb = a.stride[0]; p.dq_sh = a.stride[1]; p.dq_sn = a.stride[2];
+  a = to_t4(dk); p.dk = dk->data; p.dk_sb = a.stride[0]; p.dk_sh = a.stride[1]; p.dk_sn = a.stride[2];
+  a = to_t4(dv); p.dv = dv->data; p.dv_sb = a.stride[0]; p.dv_sh = a.stride[1]; p.dv_sn = a.stride[2];
+  if (duq) {
+    if (duq->dtype != FB_F32 || duk->dtype != FB_F32) return fail(FB_EVALUE, "factor gradients are fp32");
+    a = to_t4(duq); p.duq = (float*)duq->data; p.duq_sb = a.stride[0]; p.duq_sh = a.stride[1]; p.duq_sn = a.stride[2];
+    a = to_t4(duk); p.duk = (float*)duk->data; p.duk_sb = a.stride[0]; p.duk_sh = a.stride[1]; p.duk_sn = a.stride[2];
+  }
+  if (uq) {
+    p.uq_bb = uq->shape[0] == 1; p.uq_hb = uq->shape[1] == 1;
+    p.uk_bb = uk->shape[0] == 1; p.uk_hb = uk->shape[1] == 1;
+  }
+  if (bias) { p.bias_bb = bias->shape[0] == 1; p.bias_hb = bias->shape[1] == 1; }
+  e = launch_bwd_sm100(D, rp, bias != nullptr, q->dtype == FB_BF16, duq != nullptr, maps, p, s);
+  note_launch(2);
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "bwd_sm100");
+}
+
+int fb_bwd_preprocess(const fb_tensor* o, const fb_tensor* dout, fb_tensor* delta, void* stream) {
+  if (!o || !dout || !delta) return fail(FB_EVALUE, "null tensor");
+  cudaError_t e = launch_bwd_preprocess(to_t4(o), to_t4(dout), to_t4(delta), reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "bwd_preprocess");
+}
+
+int fb_prepare_factors(const fb_tensor* f, int side, int split, float premul, fb_tensor* out, void* stream) {
+  if (!f || !out) return fail(FB_EVALUE, "null tensor");
+  if (split < 1 || split > 3) return fail(FB_EVALUE, "split must be 1, 2 or 3");
+  if (side != 0 && side != 1) return fail(FB_EVALUE, "side must be 0 (query) or 1 (key)");
+  if (out->dtype != FB_BF16 && out->dtype != FB_F16) return fail(FB_EVALUE, "panels are bf16/f16");
+  if (f->shape[3] < 1) return fail(FB_ESHAPE, "factored bias requires rank >= 1");
+  if (out->shape[3] < fb_factor_cols(f->shape[3], split)) return fail(FB_ESHAPE, "panel too narrow");
+  if (out->shape[2] != f->shape[2]) return fail(FB_ESHAPE, "panel rows differ from factor rows");
+  cudaError_t e = launch_prepare_factors(to_t4(f), side, split, premul, to_t4(out), reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "prepare_factors");
+}
+
+int fb_fold_factor_grads(const fb_tensor* dpanel, int side, int split, float postmul, fb_tensor* out, void* stream) {
+  if (!dpanel || !out) return fail(FB_EVALUE, "null tensor");
+  if (split < 1 || split > 3) return fail(FB_EVALUE, "split must be 1, 2 or 3");
+  if (dpanel->shape[3] < fb_factor_cols(out->shape[3], split)) return fail(FB_ESHAPE, "panel too narrow");
+  cudaError_t e = launch_fold_factor_grads(to_t4(dpanel), side, split, postmul, to_t4(out), reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "fold_factor_grads");
+}
+
+int fb_factor_alibi(const float* slopes, int64_t heads, int64_t n, int64_t m, fb_tensor* fq, fb_tensor* fk, void* stream) {
+  if (n < 1 || m < 1) return fail(FB_EVALUE, "decompose_alibi requires n, m >= 1");
+  if (!slopes || !fq || !fk) return fail(FB_EVALUE, "null argument");
+  if (fq->shape[2] != n || fk->shape[2] != m || fq->shape[3] != 2 || fk->shape[3] != 2 || fq->shape[1] != heads)
+    return fail(FB_ESHAPE, "alibi factor outputs must be [1,H,N,2] / [1,H,M,2]");
+  cudaError_t e = launch_factor_alibi(slopes, heads, n, m, to_t4(fq), to_t4(fk), reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "factor_alibi");
+}
+
+int fb_factor_spatial(const fb_tensor* pos_q, const fb_tensor* pos_k, const fb_tensor* w, fb_tensor* fq, fb_tensor* fk,
+                      void* stream) {
+  if (!pos_q || !pos_k || !fq || !fk) return fail(FB_EVALUE, "null argument");
+  if (pos_q->shape[3] != 3 || pos_k->shape[3] != 3) return fail(FB_ESHAPE, "decompose_spatial requires N x 3 positions");
+  if (fq->shape[3] != 9 || fk->shape[3] != 9) return fail(FB_ESHAPE, "spatial factors have rank 9");
+  if (w && w->shape[3] != pos_q->shape[2]) return fail(FB_ESHAPE, "row_weights length must equal pos_q rows");
+  Tensor4 tw = w ? to_t4(w) : Tensor4{};
+  cudaError_t e = launch_factor_spatial(to_t4(pos_q), to_t4(pos_k), w ? &tw : nullptr, to_t4(fq), to_t4(fk),
+                                        reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "factor_spatial");
+}
+
+int fb_dense_from_factors(const fb_tensor* fq, const fb_tensor* fk, fb_tensor* out, void* stream) {
+  if (!fq || !fk || !out) return fail(FB_EVALUE, "null argument");
+  if (fq->shape[3] != fk->shape[3]) return fail(FB_ESHAPE, "factor ranks differ");
+  if (fq->shape[3] > 64) return fail(FB_ECONFIG, "rank > 64 not supported");
+  if (out->shape[2] != fq->shape[2] || out->shape[3] != fk->shape[2]) return fail(FB_ESHAPE, "output shape mismatch");
+  cudaError_t e = launch_dense_from_factors(to_t4(fq), to_t4(fk), to_t4(out), reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "dense_from_factors");
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// fb_kernels.h — internal launch interfaces between the C ABI (fb_capi.cu)
+// and the kernels.  Not part of the public boundary (include/flashbias_b200.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+
+namespace fb {
+
+struct FwdParams {
+  int B, H, N, M;
+  int causal;
+  int num_pairs;      // ceil(N / 256): CTAs per (b,h)
+  float scale_log2;   // softmax scale * log2(e)
+  void* o;            // [B,H,N,D] output (element strides below)
+  int64_t o_sb, o_sh, o_sn;
+  float* lse;         // [B,H,N] contiguous, natural-log units (nullable)
+  int uq_bb, uq_hb;   // factor / bias broadcast flags (size-1 dims)
+  int uk_bb, uk_hb;
+  int bias_bb, bias_hb;
+};
+
+struct FwdMaps {
+  CUtensorMap q, k, v, uq, uk, bias;
+};
+
+cudaError_t launch_fwd_sm100(int d, int rp, bool dense, bool bf16, const FwdMaps& maps,
+                             const FwdParams& p, cudaStream_t s);
+
+// ----- backward (tcgen05): dK'/dV (KV-stationary) and dQ' (Q-stationary)
+struct BwdParams {
+  int B, H, N, M;
+  int causal;
+  float scale;        // softmax scale
+  float scale_log2;   // scale * log2(e)
+  const float* lse;   // [B,H,N] natural-log
+  const float* delta; // [B,H,N] rowsum(dO * O)
+  void* dq; int64_t dq_sb, dq_sh, dq_sn;
+  void* dk; int64_t dk_sb, dk_sh, dk_sn;
+  void* dv; int64_t dv_sb, dv_sh, dv_sn;
+  float* duq; int64_t duq_sb, duq_sh, duq_sn;  // nullable, fp32 [B,H,N,Rpad]
+  float* duk; int64_t duk_sb, duk_sh, duk_sn;
+  int uq_bb, uq_hb, uk_bb, uk_hb, bias_bb, bias_hb;
+};
+
+struct BwdMaps {
+  // dKV kernel: streamed 64-row query-side boxes, resident 128-row key side
+  CUtensorMap q64, do64, uq64, biasT, k128, v128, uk128;
+  // dQ kernel: resident 128-row query side, streamed 64-row key-side boxes
+  CUtensorMap q128, do128, uq128, bias, k64, v64, uk64;
+};
+
+cudaError_t launch_bwd_sm100(int d, int rp, bool dense, bool bf16, bool factor_grads,
+                             const BwdMaps& maps, const BwdParams& p, cudaStream_t s);
+
+// ----- SIMT fp32 path (K5)
+struct SimtParams {
+  int B, H, N, M, D, R;
+  int causal;
+  float scale;
+  const float* q; int64_t q_sb, q_sh, q_sn;
+  const float* k; int64_t k_sb, k_sh, k_sn;
+  const float* v; int64_t v_sb, v_sh, v_sn;
+  const float* uq; int64_t uq_sb, uq_sh, uq_sn;  // nullable (R == 0)
+  const float* uk; int64_t uk_sb, uk_sh, uk_sn;
+  const float* bias; int64_t bias_sb, bias_sh, bias_sn;  // nullable
+  float* o; int64_t o_sb, o_sh, o_sn;
+  float* lse;  // nullable, [B,H,N]
+};
+cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s);
+
+// ----- small kernels
+struct Tensor4 {
+  void* data;
+  int64_t shape[4];
+  int64_t stride[4];
+  int dtype;
+};
+cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul,
+                                   const Tensor4& out, cudaStream_t s);
+cudaError_t launch_fold_factor_grads(const Tensor4& dpanel, int side, int split, float postmul,
+                                     const Tensor4& out, cudaStream_t s);
+cudaError_t launch_factor_alibi(const float* slopes, int64_t heads, int64_t n, int64_t m,
+                                const Tensor4& fq, const Tensor4& fk, cudaStream_t s);
+cudaError_t launch_factor_spatial(const Tensor4& pq, const Tensor4& pk, const Tensor4* w,
+                                  const Tensor4& fq, const Tensor4& fk, cudaStream_t s);
+cudaError_t launch_dense_from_factors(const Tensor4& fq, const Tensor4& fk, const Tensor4& out,
+                                      cudaStream_t s);
+cudaError_t launch_bwd_preprocess(const Tensor4& o, const Tensor4& dout, const Tensor4& delta,
+                                  cudaStream_t s);
+
+int factor_pairs(int split);
+
+// launch accounting (fb_launch_count)
+void note_launch(int n = 1);
+
+}  // namespace fb

@@ -1,0 +1,388 @@
+// fb_small.cu — the HBM-bound helper kernels of the path:
+//   K6  closed-form factors (ALiBi, spatial) and the bf16 k-way factor split
+//       (+ its inverse for factor gradients),
+//   K8  dense bias from factors (dense-baseline input),
+//   the backward preprocess D = rowsum(dO * O),
+//   K5  the fp32 SIMT attention forward (config C1, parity 1e-5).
+#include <math.h>
+
+#include "fb_kernels.h"
+#include "fb_sm100.cuh"
+
+namespace fb {
+
+// ------------------------------------------------------------ element access
+__device__ __forceinline__ float load_elem(const void* p, int64_t i, int dtype) {
+  switch (dtype) {
+    case 0: return reinterpret_cast<const float*>(p)[i];
+    case 1: return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+    case 2: return __half2float(reinterpret_cast<const __half*>(p)[i]);
+    default: return static_cast<float>(reinterpret_cast<const double*>(p)[i]);
+  }
+}
+__device__ __forceinline__ void store_elem(void* p, int64_t i, int dtype, float v) {
+  switch (dtype) {
+    case 0: reinterpret_cast<float*>(p)[i] = v; break;
+    case 1: reinterpret_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(v); break;
+    case 2: reinterpret_cast<__half*>(p)[i] = __float2half_rn(v); break;
+    default: reinterpret_cast<double*>(p)[i] = v; break;
+  }
+}
+__device__ __forceinline__ float round_to(float x, int dtype) {
+  return dtype == 1 ? __bfloat162float(__float2bfloat16_rn(x)) : __half2float(__float2half_rn(x));
+}
+__device__ __forceinline__ int64_t off4(const Tensor4& t, int64_t b, int64_t h, int64_t l, int64_t c) {
+  return b * t.stride[0] + h * t.stride[1] + l * t.stride[2] + c * t.stride[3];
+}
+
+int factor_pairs(int split) { return split * (split + 1) / 2; }
+
+// pair index -> (a, b) with a + b <= split-1, ordered by total then a
+__device__ __forceinline__ void pair_parts(int pidx, int& a, int& b) {
+  int tot = 0, base = 0;
+  while (pidx >= base + tot + 1) {
+    base += tot + 1;
+    ++tot;
+  }
+  a = pidx - base;
+  b = tot - a;
+}
+
+// part_i(x): successive residual roundings of x to the panel dtype
+__device__ __forceinline__ float split_part(float x, int part, int dtype) {
+  float rem = x, cur = 0.f;
+  for (int i = 0; i <= part; ++i) {
+    cur = round_to(rem, dtype);
+    rem = rem - cur;
+  }
+  return cur;
+}
+
+// ------------------------------------------------------------ K6 split
+__global__ void prepare_factors_kernel(Tensor4 f, int side, int split, float premul, Tensor4 out) {
+  const int R = static_cast<int>(f.shape[3]);
+  const int np = (split * (split + 1)) / 2;
+  const int64_t L = out.shape[2], Hh = out.shape[1], Bb = out.shape[0];
+  const int64_t rpad = out.shape[3];
+  const int64_t total = Bb * Hh * L * rpad;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = idx % rpad;
+    const int64_t l = (idx / rpad) % L;
+    const int64_t h = (idx / (rpad * L)) % Hh;
+    const int64_t b = idx / (rpad * L * Hh);
+    float v = 0.f;
+    if (c < static_cast<int64_t>(R) * np) {
+      const int r = static_cast<int>(c / np);
+      int a, bpart;
+      pair_parts(static_cast<int>(c % np), a, bpart);
+      const float x = load_elem(f.data, off4(f, b, h, l, r), f.dtype) * (side == 0 ? premul : 1.0f);
+      v = split_part(x, side == 0 ? a : bpart, out.dtype);
+    }
+    store_elem(out.data, off4(out, b, h, l, c), out.dtype, v);
+  }
+}
+
+cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul,
+                                   const Tensor4& out, cudaStream_t s) {
+  const int64_t total = out.shape[0] * out.shape[1] * out.shape[2] * out.shape[3];
+  const int grid = static_cast<int>((total + 255) / 256 > 148 * 16 ? 148 * 16 : (total + 255) / 256);
+  prepare_factors_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(f, side, split, premul, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// inverse: sum the columns whose own part index is 0 (they pair with every
+// partner part, so their gradient sums to d/d(logical factor)), reduce over
+// broadcast batch/head dims.
+__global__ void fold_factor_grads_kernel(Tensor4 dp, int side, int split, float postmul, Tensor4 out) {
+  const int np = (split * (split + 1)) / 2;
+  const int64_t R = out.shape[3], L = out.shape[2], Ho = out.shape[1], Bo = out.shape[0];
+  const int64_t Hi = dp.shape[1], Bi = dp.shape[0];
+  const int64_t total = Bo * Ho * L * R;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx % R;
+    const int64_t l = (idx / R) % L;
+    const int64_t ho = (idx / (R * L)) % Ho;
+    const int64_t bo = idx / (R * L * Ho);
+    float acc = 0.f;
+    for (int64_t bi = (Bo == 1 ? 0 : bo); bi < (Bo == 1 ? Bi : bo + 1); ++bi)
+      for (int64_t hi = (Ho == 1 ? 0 : ho); hi < (Ho == 1 ? Hi : ho + 1); ++hi)
+        for (int pidx = 0; pidx < np; ++pidx) {
+          int a, b;
+          pair_parts(pidx, a, b);
+          if ((side == 0 ? a : b) != 0) continue;
+          acc += load_elem(dp.data, off4(dp, bi, hi, l, r * np + pidx), dp.dtype);
+        }
+    store_elem(out.data, off4(out, bo, ho, l, r), out.dtype, acc * postmul);
+  }
+}
+
+cudaError_t launch_fold_factor_grads(const Tensor4& dpanel, int side, int split, float postmul,
+                                     const Tensor4& out, cudaStream_t s) {
+  const int64_t total = out.shape[0] * out.shape[1] * out.shape[2] * out.shape[3];
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  fold_factor_grads_kernel<<<g > 0 ? static_cast<int>(g) : 1, 256, 0, s>>>(dpanel, side, split, postmul, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ closed forms
+// decompose.py:37-52 — fq[i] = slope*[1, i], fk[j] = [-j, 1] over 1-based i, j
+__global__ void alibi_kernel(const float* slopes, int64_t heads, int64_t n, int64_t m, Tensor4 fq,
+                             Tensor4 fk) {
+  const int64_t total = heads * (n + m);
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t h = idx / (n + m);
+    const int64_t t = idx % (n + m);
+    if (t < n) {
+      const float s = slopes[h];
+      store_elem(fq.data, off4(fq, 0, h, t, 0), fq.dtype, s);
+      store_elem(fq.data, off4(fq, 0, h, t, 1), fq.dtype, s * static_cast<float>(t + 1));
+    } else {
+      const int64_t j = t - n;
+      store_elem(fk.data, off4(fk, 0, h, j, 0), fk.dtype, -static_cast<float>(j + 1));
+      store_elem(fk.data, off4(fk, 0, h, j, 1), fk.dtype, 1.0f);
+    }
+  }
+}
+
+cudaError_t launch_factor_alibi(const float* slopes, int64_t heads, int64_t n, int64_t m,
+                                const Tensor4& fq, const Tensor4& fk, cudaStream_t s) {
+  int64_t g = (heads * (n + m) + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  alibi_kernel<<<static_cast<int>(g), 256, 0, s>>>(slopes, heads, n, m, fq, fk);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// decompose.py:55-81 — per coordinate d: fq += [x_d^2, 1, -2 x_d], fk += [1, y_d^2, y_d],
+// fq row scaled by the row weight.
+__global__ void spatial_kernel(Tensor4 pq, Tensor4 pk, Tensor4 w, int has_w, Tensor4 fq, Tensor4 fk) {
+  const int64_t Bq = fq.shape[0], Hq = fq.shape[1], N = fq.shape[2];
+  const int64_t Bk = fk.shape[0], Hk = fk.shape[1], M = fk.shape[2];
+  const int64_t tq = Bq * Hq * N, tk = Bk * Hk * M;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < tq + tk;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (idx < tq) {
+      const int64_t i = idx % N, h = (idx / N) % Hq, b = idx / (N * Hq);
+      const int64_t pb = pq.shape[0] == 1 ? 0 : b, ph = pq.shape[1] == 1 ? 0 : h;
+      float wt = 1.f;
+      if (has_w) wt = load_elem(w.data, off4(w, w.shape[0] == 1 ? 0 : b, w.shape[1] == 1 ? 0 : h, 0, i) , w.dtype);
+      for (int d = 0; d < 3; ++d) {
+        const float x = load_elem(pq.data, off4(pq, pb, ph, i, d), pq.dtype);
+        store_elem(fq.data, off4(fq, b, h, i, 3 * d + 0), fq.dtype, wt * x * x);
+        store_elem(fq.data, off4(fq, b, h, i, 3 * d + 1), fq.dtype, wt);
+        store_elem(fq.data, off4(fq, b, h, i, 3 * d + 2), fq.dtype, wt * -2.0f * x);
+      }
+    } else {
+      const int64_t k = idx - tq;
+      const int64_t j = k % M, h = (k / M) % Hk, b = k / (M * Hk);
+      const int64_t pb = pk.shape[0] == 1 ? 0 : b, ph = pk.shape[1] == 1 ? 0 : h;
+      for (int d = 0; d < 3; ++d) {
+        const float y = load_elem(pk.data, off4(pk, pb, ph, j, d), pk.dtype);
+        store_elem(fk.data, off4(fk, b, h, j, 3 * d + 0), fk.dtype, 1.0f);
+        store_elem(fk.data, off4(fk, b, h, j, 3 * d + 1), fk.dtype, y * y);
+        store_elem(fk.data, off4(fk, b, h, j, 3 * d + 2), fk.dtype, y);
+      }
+    }
+  }
+}
+
+cudaError_t launch_factor_spatial(const Tensor4& pq, const Tensor4& pk, const Tensor4* w,
+                                  const Tensor4& fq, const Tensor4& fk, cudaStream_t s) {
+  const int64_t total = fq.shape[0] * fq.shape[1] * fq.shape[2] + fk.shape[0] * fk.shape[1] * fk.shape[2];
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 8) g = 148 * 8;
+  Tensor4 wz = w ? *w : pq;
+  spatial_kernel<<<static_cast<int>(g), 256, 0, s>>>(pq, pk, wz, w ? 1 : 0, fq, fk);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ K8 dense bias
+// out[b,h,i,j] = sum_r fq[b,h,i,r] fk[b,h,j,r]  (fp32 FMA, one pass, coalesced along j)
+__global__ void dense_from_factors_kernel(Tensor4 fq, Tensor4 fk, Tensor4 out) {
+  const int64_t Bo = out.shape[0], Ho = out.shape[1], N = out.shape[2], M = out.shape[3];
+  const int R = static_cast<int>(fq.shape[3]);
+  const int64_t rows = Bo * Ho * N;
+  for (int64_t rowi = blockIdx.x; rowi < rows; rowi += gridDim.x) {
+    const int64_t i = rowi % N, h = (rowi / N) % Ho, b = rowi / (N * Ho);
+    const int64_t qb = fq.shape[0] == 1 ? 0 : b, qh = fq.shape[1] == 1 ? 0 : h;
+    const int64_t kb = fk.shape[0] == 1 ? 0 : b, kh = fk.shape[1] == 1 ? 0 : h;
+    float a[64];
+    for (int r = 0; r < R && r < 64; ++r) a[r] = load_elem(fq.data, off4(fq, qb, qh, i, r), fq.dtype);
+    for (int64_t j = threadIdx.x; j < M; j += blockDim.x) {
+      float acc = 0.f;
+      for (int r = 0; r < R && r < 64; ++r) acc = fmaf(a[r], load_elem(fk.data, off4(fk, kb, kh, j, r), fk.dtype), acc);
+      store_elem(out.data, off4(out, b, h, i, j), out.dtype, acc);
+    }
+  }
+}
+
+cudaError_t launch_dense_from_factors(const Tensor4& fq, const Tensor4& fk, const Tensor4& out,
+                                      cudaStream_t s) {
+  if (fq.shape[3] > 64) return cudaErrorInvalidValue;
+  const int64_t rows = out.shape[0] * out.shape[1] * out.shape[2];
+  const int grid = static_cast<int>(rows < 148 * 64 ? rows : 148 * 64);
+  dense_from_factors_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(fq, fk, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ bwd preprocess
+__global__ void bwd_preprocess_kernel(Tensor4 o, Tensor4 dout, Tensor4 delta) {
+  const int64_t B = o.shape[0], H = o.shape[1], N = o.shape[2], D = o.shape[3];
+  const int64_t rows = B * H * N;
+  const int warps = blockDim.x / 32;
+  for (int64_t row = blockIdx.x * static_cast<int64_t>(warps) + threadIdx.x / 32; row < rows;
+       row += static_cast<int64_t>(gridDim.x) * warps) {
+    const int64_t i = row % N, h = (row / N) % H, b = row / (N * H);
+    float acc = 0.f;
+    for (int64_t c = threadIdx.x & 31; c < D; c += 32)
+      acc += load_elem(o.data, off4(o, b, h, i, c), o.dtype) * load_elem(dout.data, off4(dout, b, h, i, c), dout.dtype);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if ((threadIdx.x & 31) == 0) reinterpret_cast<float*>(delta.data)[(b * H + h) * N + i] = acc;
+  }
+}
+
+cudaError_t launch_bwd_preprocess(const Tensor4& o, const Tensor4& dout, const Tensor4& delta,
+                                  cudaStream_t s) {
+  const int64_t rows = o.shape[0] * o.shape[1] * o.shape[2];
+  int64_t g = (rows + 7) / 8;
+  if (g > 148 * 16) g = 148 * 16;
+  bwd_preprocess_kernel<<<static_cast<int>(g), 256, 0, s>>>(o, dout, delta);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ K5 fp32 SIMT forward
+// One warp per 4 query rows, 16 rows per CTA; K'/V tiles of 32 rows in smem.
+// Scores use exact fp32 FMA over the widened channels [q | uq] . [k | uk]
+// (attention.py:186 with the factor columns of 225-230) and expf, so the
+// result tracks the f64 reference to ~1e-6 relative.
+constexpr int kSimtRows = 16;
+constexpr int kSimtKv = 32;
+
+__global__ void __launch_bounds__(128) fwd_simt_f32_kernel(const SimtParams p) {
+  extern __shared__ float sm[];
+  const int DK = p.D + p.R;
+  const int DKP = DK | 1;  // odd stride: conflict-free column walks
+  float* sQ = sm;                                // [16][DK]
+  float* sK = sQ + kSimtRows * DK;               // [32][DKP]
+  float* sV = sK + kSimtKv * DKP;                // [32][D]
+  const int b = blockIdx.z, h = blockIdx.y;
+  const int q0 = blockIdx.x * kSimtRows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int idx = threadIdx.x; idx < kSimtRows * DK; idx += blockDim.x) {
+    const int r = idx / DK, c = idx % DK, row = q0 + r;
+    float v = 0.f;
+    if (row < p.N) {
+      if (c < p.D) v = p.q[b * p.q_sb + h * p.q_sh + static_cast<int64_t>(row) * p.q_sn + c];
+      else v = p.uq[b * p.uq_sb + h * p.uq_sh + static_cast<int64_t>(row) * p.uq_sn + (c - p.D)];
+    }
+    sQ[idx] = v;
+  }
+
+  // logits and the running max are kept in fp64 so large additive biases
+  // (ALiBi offsets of several hundred) do not cost fp32 ulps in exp(s - m)
+  double m_run[4];
+  float l_run[4], acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m_run[i] = -INFINITY;
+    l_run[i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+  }
+  int kv_end = p.M;
+  if (p.causal) kv_end = min(p.M, q0 + kSimtRows);
+  for (int kv0 = 0; kv0 < kv_end; kv0 += kSimtKv) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < kSimtKv * DK; idx += blockDim.x) {
+      const int r = idx / DK, c = idx % DK, j = kv0 + r;
+      float v = 0.f;
+      if (j < p.M) {
+        if (c < p.D) v = p.k[b * p.k_sb + h * p.k_sh + static_cast<int64_t>(j) * p.k_sn + c];
+        else v = p.uk[b * p.uk_sb + h * p.uk_sh + static_cast<int64_t>(j) * p.uk_sn + (c - p.D)];
+      }
+      sK[r * DKP + c] = v;
+    }
+    for (int idx = threadIdx.x; idx < kSimtKv * p.D; idx += blockDim.x) {
+      const int r = idx / p.D, c = idx % p.D, j = kv0 + r;
+      sV[idx] = j < p.M ? p.v[b * p.v_sb + h * p.v_sh + static_cast<int64_t>(j) * p.v_sn + c] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = warp * 4 + i, row = q0 + r;
+      const int j = kv0 + lane;
+      float s = 0.f;
+      const float* qr = sQ + r * DK;
+      const float* kr = sK + lane * DKP;
+      for (int c = 0; c < p.D; ++c) s = fmaf(qr[c], kr[c], s);
+      double su = 0.0;
+      for (int c = p.D; c < DK; ++c) su = fma(static_cast<double>(qr[c]), static_cast<double>(kr[c]), su);
+      double sd = (static_cast<double>(s) + su) * static_cast<double>(p.scale);
+      if (p.bias && j < p.M && row < p.N)
+        sd += p.bias[b * p.bias_sb + h * p.bias_sh + static_cast<int64_t>(row) * p.bias_sn + j];
+      if (j >= p.M || (p.causal && j > row)) sd = -INFINITY;
+      double mx = sd;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const double m_new = fmax(m_run[i], mx);
+      if (m_new == -INFINITY) continue;  // nothing visible yet in this row
+      const float alpha = expf(static_cast<float>(m_run[i] - m_new));
+      const float pj = expf(static_cast<float>(sd - m_new));
+      float ps = pj;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      l_run[i] = l_run[i] * alpha + ps;
+      m_run[i] = m_new;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[i][c] *= alpha;
+      for (int jj = 0; jj < kSimtKv; ++jj) {
+        const float pb = __shfl_sync(0xffffffffu, pj, jj);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int col = lane + 32 * c;
+          if (col < p.D) acc[i][c] = fmaf(pb, sV[jj * p.D + col], acc[i][c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = q0 + warp * 4 + i;
+    if (row >= p.N) continue;
+    const float inv = 1.0f / l_run[i];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int col = lane + 32 * c;
+      if (col < p.D) p.o[b * p.o_sb + h * p.o_sh + static_cast<int64_t>(row) * p.o_sn + col] = acc[i][c] * inv;
+    }
+    if (p.lse && lane == 0) p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + row] = static_cast<float>(m_run[i] + log(static_cast<double>(l_run[i])));
+  }
+}
+
+cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s) {
+  const int DK = p.D + p.R;
+  const size_t smem = sizeof(float) * (kSimtRows * DK + kSimtKv * (DK | 1) + kSimtKv * p.D);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((p.N + kSimtRows - 1) / kSimtRows, p.H, p.B);
+  fwd_simt_f32_kernel<<<grid, 128, smem, s>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace fb

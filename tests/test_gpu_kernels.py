@@ -1,0 +1,164 @@
+"""GPU numerics of the sm_100a kernels against a plain torch float64 reference
+of the same op (materialised softmax).  Tolerances are the north-star ones:
+bf16/fp16 2e-2 relative (max-abs / max|ref|), fp32 1e-5 relative."""
+
+import math
+
+import pytest
+import torch
+
+import paper_2505_12044_b200 as fb
+from paper_2505_12044_b200 import attention as A
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+F32_TOL = 1e-5
+
+
+def ref_attention(q, k, v, fq=None, fk=None, bias=None, causal=False, scale=None):
+    qd, kd, vd = q.double(), k.double(), v.double()
+    scale = scale if scale is not None else 1.0 / math.sqrt(q.shape[-1])
+    s = qd @ kd.transpose(-1, -2) * scale
+    if fq is not None:
+        s = s + fq.double() @ fk.double().transpose(-1, -2)
+    if bias is not None:
+        s = s + bias.double()
+    if causal:
+        m = torch.ones(s.shape[-2], s.shape[-1], dtype=torch.bool, device=s.device).triu(1)
+        s = s.masked_fill(m, float("-inf"))
+    return torch.softmax(s, -1) @ vd
+
+
+def relerr(a, b):
+    return float((a.double() - b.double()).abs().max() / b.double().abs().max().clamp_min(1e-30))
+
+
+def _qkv(B, H, N, M, D, dtype, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = torch.randn(B, H, N, D, device="cuda", generator=g).to(dtype)
+    k = torch.randn(B, H, M, D, device="cuda", generator=g).to(dtype)
+    v = torch.randn(B, H, M, D, device="cuda", generator=g).to(dtype)
+    return q, k, v
+
+
+@pytest.mark.parametrize("D", [32, 64, 128])
+@pytest.mark.parametrize("N,M,causal", [(256, 256, False), (384, 384, True), (200, 333, False), (77, 77, True)])
+def test_fwd_nobias(D, N, M, causal):
+    q, k, v = _qkv(2, 3, N, M, D, torch.bfloat16)
+    out = fb.tiled_attention(q, k, v, mask="causal" if causal else "none")
+    ref = ref_attention(q, k, v, causal=causal)
+    assert out.dtype == torch.bfloat16 and out.shape == q.shape
+    assert relerr(out, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("R", [2, 9, 16, 64])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fwd_factored(D, R, causal):
+    N = 384
+    q, k, v = _qkv(1, 2, N, N, D, torch.bfloat16, seed=R)
+    g = torch.Generator(device="cuda").manual_seed(100 + R)
+    fq = torch.randn(1, 2, N, R, device="cuda", generator=g) * 0.5
+    fk = torch.randn(1, 2, N, R, device="cuda", generator=g) * 0.5
+    if R == 64:  # rank 64 only fits unsplit panels: feed bf16-exact factors
+        fq, fk = fq.bfloat16().float(), fk.bfloat16().float()
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask="causal" if causal else "none")
+    ref = ref_attention(q, k, v, fq, fk, causal=causal)
+    assert relerr(out, ref) < BF16_TOL
+
+
+def test_fwd_alibi_long_split():
+    N, H = 2048, 4
+    q, k, v = _qkv(1, H, N, N, 128, torch.bfloat16, seed=5)
+    slopes = [-(2.0 ** (-8.0 * (h + 1) / H)) for h in range(H)]
+    fq, fk = fb.alibi_factors(slopes, N, N)
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask="causal")
+    i = torch.arange(1, N + 1, device="cuda", dtype=torch.float64)
+    dense = torch.tensor(slopes, device="cuda", dtype=torch.float64)[:, None, None] * (i[:, None] - i[None, :])
+    ref = ref_attention(q, k, v, bias=dense[None], causal=True)
+    assert relerr(out, ref) < BF16_TOL
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_fwd_dense_bias(D, causal):
+    N = 320
+    q, k, v = _qkv(2, 2, N, N, D, torch.bfloat16, seed=9)
+    bias = (torch.randn(1, 2, N, N, device="cuda") * 2).bfloat16()
+    out = fb.tiled_attention(q, k, v, fb.DenseBias(bias), mask="causal" if causal else "none")
+    ref = ref_attention(q, k, v, bias=bias, causal=causal)
+    assert relerr(out, ref) < BF16_TOL
+
+
+def test_fwd_fp16():
+    q, k, v = _qkv(1, 2, 256, 256, 64, torch.float16, seed=3)
+    fq = torch.randn(1, 2, 256, 4, device="cuda")
+    fk = torch.randn(1, 2, 256, 4, device="cuda")
+    out = fb.flashbias_attention(q, k, v, fq, fk)
+    assert relerr(out, ref_attention(q, k, v, fq, fk)) < BF16_TOL
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_fwd_fp32_simt(causal):
+    q, k, v = _qkv(1, 8, 1024, 1024, 64, torch.float32, seed=11)
+    fq, fk = fb.alibi_factors([-(2.0 ** -(h + 1)) for h in range(8)], 1024, 1024)
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask="causal" if causal else "none")
+    ref = ref_attention(q, k, v, fq, fk, causal=causal)
+    assert out.dtype == torch.float32
+    assert relerr(out, ref) < F32_TOL
+
+
+def _bwd_case(B, H, N, M, D, R, causal, dense=False, seed=0):
+    q, k, v = _qkv(B, H, N, M, D, torch.bfloat16, seed=seed)
+    q.requires_grad_(True)
+    k.requires_grad_(True)
+    v.requires_grad_(True)
+    fq = fk = bias = None
+    if R:
+        g = torch.Generator(device="cuda").manual_seed(seed + 7)
+        fq = (torch.randn(1, H, N, R, device="cuda", generator=g) * 0.5).requires_grad_(True)
+        fk = (torch.randn(1, H, M, R, device="cuda", generator=g) * 0.5).requires_grad_(True)
+    if dense:
+        bias = (torch.randn(1, H, N, M, device="cuda") * 2).bfloat16()
+    do = torch.randn(B, H, N, D, device="cuda").bfloat16()
+    mask = "causal" if causal else "none"
+    if R:
+        out = fb.flashbias_attention(q, k, v, fq, fk, mask=mask)
+    elif dense:
+        out = fb.tiled_attention(q, k, v, fb.DenseBias(bias), mask=mask)
+    else:
+        out = fb.tiled_attention(q, k, v, mask=mask)
+    out.backward(do)
+    leaves = [q, k, v] + ([fq, fk] if R else [])
+    got = [t.grad.clone() for t in leaves]
+    ref_leaves = [t.detach().double().requires_grad_(True) for t in leaves]
+    rq, rk, rv = ref_leaves[:3]
+    rfq, rfk = (ref_leaves[3], ref_leaves[4]) if R else (None, None)
+    ref = ref_attention(rq, rk, rv, rfq, rfk, bias=bias, causal=causal)
+    ref.backward(do.double())
+    for name, g_, r_ in zip(["dq", "dk", "dv", "dfq", "dfk"], got, ref_leaves):
+        e = relerr(g_, r_.grad)
+        assert e < BF16_TOL, f"{name}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("D", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_bwd_nobias(D, causal):
+    _bwd_case(2, 2, 256, 256, D, 0, causal)
+
+
+@pytest.mark.parametrize("D,R", [(64, 9), (128, 2), (128, 16)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_bwd_factored(D, R, causal):
+    _bwd_case(2, 2, 384, 384, D, R, causal, seed=R)
+
+
+def test_bwd_ragged():
+    _bwd_case(1, 2, 200, 200, 64, 4, True, seed=1)
+    _bwd_case(1, 2, 150, 333, 64, 4, False, seed=2)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_bwd_dense(causal):
+    _bwd_case(1, 2, 256, 256, 128, 0, causal, dense=True)
