@@ -150,8 +150,8 @@ def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int =
     below ``tol`` (logit units), limited by R * k(k+1)/2 <= max_cols.
     """
     import torch
-    a = fq.float() * premul
-    b = fk.float()
+    a = fq.detach().float() * premul
+    b = fk.detach().float()
     if torch.equal(a.to(torch.bfloat16).float(), a) and torch.equal(b.to(torch.bfloat16).float(), b):
         return 1
     r = a.shape[-1]

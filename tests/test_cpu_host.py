@@ -1,0 +1,152 @@
+"""Host-side logic that needs no GPU: the C-ABI library loads and exports every
+symbol include/flashbias_b200.h declares, the Python API validates exactly
+like the reference (attention.py:77-108, 215-223; errors.py), and the
+tile-size / split helpers behave as documented."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2505_12044_b200 as fb
+from paper_2505_12044_b200 import _lib
+from paper_2505_12044_b200.errors import ConfigError, MaskError, ShapeError, ValidationError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flashbias_b200.h")
+
+
+def _header_functions():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(fb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_what_python_binds():
+    assert _header_functions() == sorted(_lib.EXPORTED_SYMBOLS)
+
+
+def test_library_loads_and_exports_every_symbol():
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("native library not built (run __graft_entry__.build())")
+    handle = ctypes.CDLL(_lib.LIB_PATH)
+    for name in _header_functions():
+        assert hasattr(handle, name), name
+    lib = _lib.lib()
+    assert lib.fb_abi_version() == 1
+    # pure host helpers of the ABI can be called without a GPU
+    assert lib.fb_factor_cols(2, 3) == 12 and lib.fb_factor_rpad(2, 3) == 16
+    assert lib.fb_factor_cols(9, 2) == 27 and lib.fb_factor_rpad(9, 2) == 32
+    assert lib.fb_factor_rpad(64, 1) == 64
+
+
+def test_abi_validation_maps_to_reference_exceptions():
+    """Shape/mask validation in the C ABI happens before any launch, so it is
+    testable on a CPU-only host with fake device pointers."""
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("native library not built")
+    lib = _lib.lib()
+
+    def t(b, h, n, d, dtype=_lib.FB_BF16):
+        x = _lib.FbTensor()
+        x.data = 4096
+        for i, s in enumerate((b, h, n, d)):
+            x.shape[i] = s
+        x.stride[3], x.stride[2], x.stride[1], x.stride[0] = 1, d, n * d, h * n * d
+        x.dtype = dtype
+        return x
+
+    q, k, v, o = t(1, 2, 64, 64), t(1, 2, 80, 64), t(1, 2, 80, 64), t(1, 2, 64, 64)
+    with pytest.raises(MaskError):
+        _lib.check(lib.fb_attn_fwd(ctypes.byref(q), ctypes.byref(k), ctypes.byref(v), None, None, None, 1,
+                                   0.125, ctypes.byref(o), None, None))
+    kbad = t(1, 2, 80, 32)
+    with pytest.raises(ShapeError):
+        _lib.check(lib.fb_attn_fwd(ctypes.byref(q), ctypes.byref(kbad), ctypes.byref(v), None, None, None, 0,
+                                   0.125, ctypes.byref(o), None, None))
+    uq, uk = t(1, 2, 64, 16), t(1, 2, 80, 32)
+    with pytest.raises(ShapeError):
+        _lib.check(lib.fb_attn_fwd(ctypes.byref(q), ctypes.byref(k), ctypes.byref(v), ctypes.byref(uq),
+                                   ctypes.byref(uk), None, 0, 0.125, ctypes.byref(o), None, None))
+    with pytest.raises(ValidationError):
+        _lib.check(lib.fb_attn_fwd(ctypes.byref(q), ctypes.byref(k), ctypes.byref(v), None, None, None, 7,
+                                   0.125, ctypes.byref(o), None, None))
+    q48, k48, v48, o48 = t(1, 2, 64, 48), t(1, 2, 64, 48), t(1, 2, 64, 48), t(1, 2, 64, 48)
+    with pytest.raises(ConfigError):  # unpadded head dim is rejected, not silently handled
+        _lib.check(lib.fb_attn_fwd(ctypes.byref(q48), ctypes.byref(k48), ctypes.byref(v48), None, None, None, 0,
+                                   0.125, ctypes.byref(o48), None, None))
+
+
+def test_python_validation_before_compute():
+    q = np.ones((3, 2))
+    with pytest.raises(MaskError):  # reference test_attention.py:65-68
+        fb.reference_attention(q, np.ones((4, 2)), np.ones((4, 2)), mask="causal")
+    with pytest.raises(MaskError):
+        fb.flashbias_attention(q, np.ones((4, 2)), np.ones((4, 2)), np.ones((3, 1)), np.ones((4, 1)),
+                               mask="causal")
+    with pytest.raises(ShapeError):
+        fb.flashbias_attention(q, np.ones((4, 3)), np.ones((4, 3)), np.ones((3, 1)), np.ones((4, 1)))
+    with pytest.raises(ShapeError):
+        fb.tiled_attention(q, np.ones((4, 2)), np.ones((5, 2)))
+    with pytest.raises(ValidationError):
+        fb.tiled_attention(q, np.ones((4, 2)), np.ones((4, 2)), mask="diagonal")
+    with pytest.raises(ValidationError):
+        fb.tiled_attention(q, np.ones((4, 2)), np.ones((4, 2)), tiles=(4, 4))
+
+
+def test_errors_are_value_errors_like_reference():
+    for cls in (ShapeError, MaskError, ConfigError, ValidationError):
+        assert issubclass(cls, ValueError)
+    e = fb.TrainingError("diverged", 17)
+    assert isinstance(e, RuntimeError) and e.iteration == 17
+
+
+def test_tile_config_and_choose_tile_sizes():
+    tiles = fb.choose_tile_sizes(64, 64, 100 * 1024, 2)  # reference test_attention.py:214-216
+    assert tiles.b_q == 96 and tiles.b_kv == 96
+    with pytest.raises(ConfigError):
+        fb.choose_tile_sizes(4096, 4096, 64, 8)
+    with pytest.raises(ConfigError):
+        fb.TileConfig(0, 4)
+    for c, r, mult in ((1, 0, 1), (64, 16, 3), (128, 128, 20)):
+        base = 4 * 8 * (c + r)
+        assert fb.choose_tile_sizes(c, r, base * mult * 2, 8).b_q >= fb.choose_tile_sizes(c, r, base * mult, 8).b_q
+
+
+def test_factored_bias_provider():
+    fq, fk = np.ones((5, 3)), np.ones((7, 3))
+    b = fb.FactoredBias(fq, fk)
+    assert b.rank == 3 and b.storage_bytes() == (5 + 7) * 3 * 8
+    assert b.dense().shape == (5, 7)
+    with pytest.raises(ShapeError):
+        fb.FactoredBias(np.ones((5, 3)), np.ones((7, 2)))
+    with pytest.raises(ValidationError):
+        fb.FactoredBias(fq, fk, origin="magic")
+    assert fb.DenseBias(np.zeros((4, 6))).storage_bytes(2) == 48
+    assert fb.NO_BIAS.storage_bytes() == 0
+
+
+def test_choose_split_levels():
+    torch = pytest.importorskip("torch")
+    # exactly representable -> no split
+    assert fb.choose_split(torch.ones(1, 1, 8, 2), torch.ones(1, 1, 8, 2)) == 1
+    # ALiBi at N=16384 with a non power-of-two slope needs the 3-way split
+    i = torch.arange(1, 16385, dtype=torch.float32)
+    s = -(2.0 ** (-8 / 32 * 3))
+    fq = torch.stack([torch.full_like(i, s), s * i], -1)[None, None]
+    fk = torch.stack([-i, torch.ones_like(i)], -1)[None, None]
+    assert fb.choose_split(fq, fk, premul=128 ** 0.5) == 3
+    # spatial factors on a normalised grid settle for 2 (27 columns -> 2 panels)
+    g = torch.rand(4096, 3)
+    w = -(0.5 + 1.5 * torch.rand(4096))
+    fq = torch.cat([w[:, None] * torch.stack([g[:, d] ** 2, torch.ones(4096), -2 * g[:, d]], -1) for d in range(3)], -1)
+    fk = torch.cat([torch.stack([torch.ones(4096), g[:, d] ** 2, g[:, d]], -1) for d in range(3)], -1)
+    assert fb.choose_split(fq[None, None], fk[None, None], premul=8.0) == 2
+
+
+def test_flashbias_alias_package():
+    import flashbias
+    assert flashbias.flashbias_attention is fb.flashbias_attention
+    assert set(["flashbias_attention", "tiled_attention", "svd_decompose", "decompose_alibi"]) <= set(flashbias.__all__)
