@@ -108,10 +108,10 @@ __global__ void __launch_bounds__(192, 1)
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + Cfg::kKVRes + Cfg::kKVSlots * Cfg::kKVSlot + 1024);
 
   const int warp = warp_id(), lane = lane_id();
-  const int bh_count = p.B * p.H;
-  const int kt = blockIdx.x / bh_count;  // ascending: causal-longest first
-  const int bh = blockIdx.x % bh_count;
-  const int b = bh / p.H, h = bh % p.H;
+  const int nkt = (p.M + 127) / 128;
+  const int kt = blockIdx.x % nkt;  // ascending: causal-longest first within a head
+  const int bh = blockIdx.x / nkt;  // head-major: resident CTAs share Q/dO via L2
+  const int h = bh / p.B, b = bh % p.B;  // a head's batches adjacent (shared bias/L2)
   const int kv0 = kt * 128;
   const int nqb = (p.N + 63) / 64;
   const int i_start = p.causal ? kv0 / 64 : 0;
@@ -381,12 +381,11 @@ __global__ void __launch_bounds__(192, 1)
   BwdBars* bars = reinterpret_cast<BwdBars*>(smem + Cfg::kQRes + Cfg::kQSlots * Cfg::kQSlot);
 
   const int warp = warp_id(), lane = lane_id();
-  const int bh_count = p.B * p.H;
   const int nqt = (p.N + 127) / 128;
-  int qt = blockIdx.x / bh_count;
-  if (p.causal) qt = nqt - 1 - qt;  // longest first
-  const int bh = blockIdx.x % bh_count;
-  const int b = bh / p.H, h = bh % p.H;
+  int qt = blockIdx.x % nqt;
+  if (p.causal) qt = nqt - 1 - qt;  // longest first within a head
+  const int bh = blockIdx.x / nqt;  // head-major: resident CTAs share K/V via L2
+  const int h = bh / p.B, b = bh % p.B;  // a head's batches adjacent (shared bias/L2)
   const int q0 = qt * 128;
   const int nkb_all = (p.M + 63) / 64;
   const int nkb = p.causal ? min(nkb_all, (q0 + 127) / 64 + 1) : nkb_all;

@@ -94,13 +94,13 @@ __global__ void __launch_bounds__(384, 1)
   const int warp = warp_id();
   const int lane = lane_id();
 
-  // ---- work decomposition: pair-major, longest (causal) pairs first
-  const int bh_count = p.B * p.H;
-  int pair = blockIdx.x / bh_count;
-  const int bh = blockIdx.x % bh_count;
+  // ---- work decomposition: head-major so the ~148 resident CTAs share the
+  // K/V of 2-3 heads through L2; within a head, longest (causal) pairs first.
+  const int bh = blockIdx.x / p.num_pairs;
+  int pair = blockIdx.x % p.num_pairs;
   if (p.causal) pair = p.num_pairs - 1 - pair;
-  const int b = bh / p.H;
-  const int h = bh % p.H;
+  const int h = bh / p.B;  // (head, batch) order: a head's batches are adjacent
+  const int b = bh % p.B;
   const int row0 = pair * 2 * kTileRows;
   int n0, n1;
   fwd_block_counts(p, pair, n0, n1);
