@@ -10,6 +10,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -21,6 +22,7 @@ namespace fb {
 
 static thread_local char g_err[512] = "";
 static thread_local int64_t g_launches = 0;
+static int g_force_split_bwd = 0;  // testing hook: FB_FORCE_SPLIT_BWD=1 selects the two-kernel backward
 
 void note_launch(int n) { g_launches += n; }
 
@@ -101,8 +103,11 @@ static int make_map(CUtensorMap* map, const fb_tensor* t, int box_cols, int box_
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                           : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                : CU_TENSOR_MAP_SWIZZLE_32B;
-  CUtensorMapDataType dt = t->dtype == FB_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUtensorMapDataType dt = t->dtype == FB_BF16  ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                           : t->dtype == FB_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUresult r = enc(map, dt, 4, t->data, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FB_ECUDA, "%s: cuTensorMapEncodeTiled failed (%d)", name, (int)r);
@@ -283,7 +288,10 @@ int fb_attn_fwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
 size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k) {
   (void)k;
   if (!q) return 0;
-  return (size_t)q->shape[0] * q->shape[1] * q->shape[2] * sizeof(float) + 256;  // delta
+  const size_t rows = (size_t)q->shape[0] * q->shape[1] * q->shape[2];
+  size_t bytes = (rows * sizeof(float) + 255) / 256 * 256 + 256;  // delta
+  if (q->shape[3] == 128) bytes += rows * 128 * sizeof(float);    // fp32 dQ accumulator (fused path)
+  return bytes;
 }
 
 int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, const fb_tensor* uq,
@@ -368,6 +376,30 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     p.uk_bb = uk->shape[0] == 1; p.uk_hb = uk->shape[1] == 1;
   }
   if (bias) { p.bias_bb = bias->shape[0] == 1; p.bias_hb = bias->shape[1] == 1; }
+  static const int force_split = [] {
+    const char* v = getenv("FB_FORCE_SPLIT_BWD");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  g_force_split_bwd = force_split;
+  const bool fused = D == 128 && duq == nullptr && !g_force_split_bwd;
+  if (fused) {
+    float* acc = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(delta) +
+                                          ((size_t)B * H * N * sizeof(float) + 255) / 256 * 256);
+    fb_tensor tacc{};
+    tacc.data = acc;
+    tacc.shape[0] = B; tacc.shape[1] = H; tacc.shape[2] = N; tacc.shape[3] = 128;
+    tacc.stride[3] = 1; tacc.stride[2] = 128; tacc.stride[1] = (int64_t)N * 128; tacc.stride[0] = (int64_t)H * N * 128;
+    tacc.dtype = FB_F32;
+    CUtensorMap macc;
+    if ((rc = make_map(&macc, &tacc, 128, 64, 0, "dq_acc"))) return rc;
+    e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * 128 * sizeof(float), s);
+    if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
+    e = launch_bwd_fused_sm100(rp, bias != nullptr, q->dtype == FB_BF16, maps, macc, p, s);
+    if (e != cudaSuccess) return cuda_fail(e, "bwd_fused_sm100");
+    e = launch_dq_convert(acc, p, q->dtype == FB_BF16, s);
+    note_launch(2);
+    return e == cudaSuccess ? FB_OK : cuda_fail(e, "dq_convert");
+  }
   e = launch_bwd_sm100(D, rp, bias != nullptr, q->dtype == FB_BF16, duq != nullptr, maps, p, s);
   note_launch(2);
   return e == cudaSuccess ? FB_OK : cuda_fail(e, "bwd_sm100");

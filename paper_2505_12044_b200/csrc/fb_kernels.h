@@ -54,6 +54,11 @@ struct BwdMaps {
 
 cudaError_t launch_bwd_sm100(int d, int rp, bool dense, bool bf16, bool factor_grads,
                              const BwdMaps& maps, const BwdParams& p, cudaStream_t s);
+// single-pass backward for d = 128 without factor gradients: dQ reduced into
+// an fp32 accumulator [B,H,N,128] through TMA bulk reductions, then converted
+cudaError_t launch_bwd_fused_sm100(int rp, bool dense, bool bf16, const BwdMaps& maps, const CUtensorMap& dqacc,
+                                   const BwdParams& p, cudaStream_t s);
+cudaError_t launch_dq_convert(const float* acc, const BwdParams& p, bool bf16, cudaStream_t s);
 
 // ----- SIMT fp32 path (K5)
 struct SimtParams {
