@@ -332,7 +332,7 @@ def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none",
                 bp = bt.contiguous()
         sp = None
         if fqt is not None:
-            sp = split or choose_split(fqt, fkt, premul)
+            sp = split or choose_split(fqt, fkt, premul, max_cols=64 if dp == 128 else 128)
         o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(scale), float(premul), sp)
         o = o[..., : vt.shape[-1]]
     return _mirror(o, shp)

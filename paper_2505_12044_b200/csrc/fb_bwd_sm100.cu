@@ -64,8 +64,8 @@ struct BwdBars {
   uint64_t p_ready;
   uint64_t ds_ready[2];
   uint64_t final_;
-  uint64_t slot_full[6];
-  uint64_t slot_empty[6];
+  uint64_t slot_full[8];
+  uint64_t slot_empty[8];
   uint32_t tmem_base;
 };
 
@@ -639,12 +639,28 @@ static cudaError_t bwd_rp(int rp, bool dense, bool fgrad, const BwdMaps& m, cons
       case 3: return launch_bwd_t<D, 3, false, BF16, true>(m, p, s);
       case 4: return launch_bwd_t<D, 4, false, BF16, true>(m, p, s);
     }
+    if constexpr (D <= 64) {
+      switch (rp) {
+        case 5: return launch_bwd_t<D, 5, false, BF16, true>(m, p, s);
+        case 6: return launch_bwd_t<D, 6, false, BF16, true>(m, p, s);
+        case 7: return launch_bwd_t<D, 7, false, BF16, true>(m, p, s);
+        case 8: return launch_bwd_t<D, 8, false, BF16, true>(m, p, s);
+      }
+    }
   } else {
     switch (rp) {
       case 1: return launch_bwd_t<D, 1, false, BF16, false>(m, p, s);
       case 2: return launch_bwd_t<D, 2, false, BF16, false>(m, p, s);
       case 3: return launch_bwd_t<D, 3, false, BF16, false>(m, p, s);
       case 4: return launch_bwd_t<D, 4, false, BF16, false>(m, p, s);
+    }
+    if constexpr (D <= 64) {
+      switch (rp) {
+        case 5: return launch_bwd_t<D, 5, false, BF16, false>(m, p, s);
+        case 6: return launch_bwd_t<D, 6, false, BF16, false>(m, p, s);
+        case 7: return launch_bwd_t<D, 7, false, BF16, false>(m, p, s);
+        case 8: return launch_bwd_t<D, 8, false, BF16, false>(m, p, s);
+      }
     }
   }
   return cudaErrorInvalidValue;

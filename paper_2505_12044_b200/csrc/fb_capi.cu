@@ -245,15 +245,17 @@ int fb_attn_fwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
   int rp = 0;
   if (uq) {
     const int64_t rpad = uq->shape[3];
-    if (rpad % 16 || rpad > 64)
-      return fail(FB_ECONFIG, "factor panels must have Rpad in {16,32,48,64} (got %lld)", (long long)rpad);
+    const int64_t rmax = D == 128 ? 64 : 128;
+    if (rpad % 16 || rpad > rmax)
+      return fail(FB_ECONFIG, "factor panels must have Rpad a multiple of 16 <= %lld for head dim %d (got %lld)",
+                  (long long)rmax, D, (long long)rpad);
     if (uq->dtype != q->dtype || uk->dtype != q->dtype) return fail(FB_EVALUE, "factor panels must match q dtype");
     rp = (int)(rpad / 16);
   }
   if (bias) {
     if (uq) return fail(FB_ECONFIG, "tcgen05 path takes either factors or a dense bias, not both");
     if (bias->dtype != q->dtype) return fail(FB_EVALUE, "dense bias dtype must match q");
-    if ((M * 2) % 16) return fail(FB_ECONFIG, "dense bias needs M to be a multiple of 8 (pad on the host)");
+    if ((bias->stride[2] * 2) % 16) return fail(FB_ECONFIG, "dense bias rows must be 16-byte aligned (pad the row stride)");
   }
   FwdMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -315,11 +317,12 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
   int rp = 0;
   if (uq) {
     const int64_t rpad = uq->shape[3];
-    if (rpad % 16 || rpad > 64) return fail(FB_ECONFIG, "factor panels must have Rpad in {16,32,48,64}");
+    if (rpad % 16 || rpad > (D == 128 ? 64 : 128))
+      return fail(FB_ECONFIG, "factor panels must have Rpad a multiple of 16 <= %d", D == 128 ? 64 : 128);
     rp = (int)(rpad / 16);
   }
   if (bias && uq) return fail(FB_ECONFIG, "either factors or a dense bias, not both");
-  if (bias && (M * 2) % 16) return fail(FB_ECONFIG, "dense bias needs M multiple of 8");
+  if (bias && (bias->stride[2] * 2) % 16) return fail(FB_ECONFIG, "dense bias rows must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // preprocess delta = rowsum(dO * O)
   float* delta = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));

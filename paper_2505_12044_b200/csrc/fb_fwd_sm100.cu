@@ -444,6 +444,14 @@ static cudaError_t dispatch_rp(int rp, bool dense, const FwdMaps& maps, const Fw
     case 3: return launch_fwd_t<D, 3, false, BF16>(maps, p, s);
     case 4: return launch_fwd_t<D, 4, false, BF16>(maps, p, s);
   }
+  if constexpr (D <= 64) {  // wider factor panels (up to 128 split columns) fit next to small heads
+    switch (rp) {
+      case 5: return launch_fwd_t<D, 5, false, BF16>(maps, p, s);
+      case 6: return launch_fwd_t<D, 6, false, BF16>(maps, p, s);
+      case 7: return launch_fwd_t<D, 7, false, BF16>(maps, p, s);
+      case 8: return launch_fwd_t<D, 8, false, BF16>(maps, p, s);
+    }
+  }
   return cudaErrorInvalidValue;
 }
 
