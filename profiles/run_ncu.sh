@@ -8,7 +8,7 @@ TAG=${1:-r01}
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:fb_ --csv \
     --log-file gpurun_out/launches_${TAG}.csv \
     python bench.py --config C3 --steps 1 --warmup 1 --skip-e2e --skip-cpu > gpurun_out/launches_${TAG}.log 2>&1
-for K in fb_fwd_kernel fb_bwd_dkv_kernel fb_bwd_dq_kernel; do
+for K in fb_fwd_kernel fb_bwd_fused_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:${K} -s 1 -c 1 \
       -o gpurun_out/prof_${TAG}_${K} -f \
       python bench.py --config C3 --steps 1 --warmup 1 --skip-dense --skip-e2e --skip-cpu > /dev/null 2>&1 || true
