@@ -17,6 +17,7 @@
 
 #include "../../include/flashbias_b200.h"
 #include "fb_kernels.h"
+#include "fb_sm100.cuh"
 
 namespace fb {
 
@@ -25,6 +26,13 @@ static thread_local int64_t g_launches = 0;
 static int g_force_split_bwd = 0;  // testing hook: FB_FORCE_SPLIT_BWD=1 selects the two-kernel backward
 
 void note_launch(int n) { g_launches += n; }
+
+static unsigned long long* g_trace_buf = nullptr;
+static int g_trace_cta = -1;
+void trace_target(unsigned long long** buf, int* cta) {
+  *buf = g_trace_buf;
+  *cta = g_trace_cta;
+}
 
 static int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -177,6 +185,15 @@ using namespace fb;
 extern "C" {
 
 const char* fb_last_error(void) { return g_err; }
+
+/* Debug hook (not part of the public header): route kernel timeline records of
+ * CTA `cta` into the device buffer `buf` (uint64, buf[0] = count).  Only the
+ * FB_TRACE=1 build records anything. */
+void fb_debug_set_trace(void* buf, int cta) {
+  g_trace_buf = reinterpret_cast<unsigned long long*>(buf);
+  g_trace_cta = cta;
+}
+int fb_debug_trace_enabled(void) { return FB_TRACE; }
 int fb_abi_version(void) { return FB_ABI_VERSION; }
 int64_t fb_launch_count(int reset) {
   const int64_t c = g_launches;
@@ -282,6 +299,7 @@ int fb_attn_fwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     p.uk_bb = uk->shape[0] == 1; p.uk_hb = uk->shape[1] == 1;
   }
   if (bias) { p.bias_bb = bias->shape[0] == 1; p.bias_hb = bias->shape[1] == 1; }
+  trace_target(&p.trace, &p.trace_cta);
   cudaError_t e = launch_fwd_sm100(D, rp, bias != nullptr, q->dtype == FB_BF16, maps, p, s);
   note_launch();
   return e == cudaSuccess ? FB_OK : cuda_fail(e, "fwd_sm100");
@@ -379,6 +397,7 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     p.uk_bb = uk->shape[0] == 1; p.uk_hb = uk->shape[1] == 1;
   }
   if (bias) { p.bias_bb = bias->shape[0] == 1; p.bias_hb = bias->shape[1] == 1; }
+  trace_target(&p.trace, &p.trace_cta);
   static const int force_split = [] {
     const char* v = getenv("FB_FORCE_SPLIT_BWD");
     return v && v[0] == '1' ? 1 : 0;

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(384, 1)
           const int slot = item % Cfg::kSlots;
           const int use = item / Cfg::kSlots;
           if (use > 0) mbar_wait(&bars->slot_empty[slot], (use - 1) & 1);
+          trace(p.trace, p.trace_cta, 20, item);
           uint8_t* dst = smem + Cfg::kQRegion + slot * Cfg::kSlotBytes;
           uint64_t* fb_ = &bars->slot_full[slot];
           if (pos == 0) {  // K (+ fk panels)
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_commit(e);
       };
       auto issue_s = [&](int t, int kitem) {
+        trace(p.trace, p.trace_cta, 2, t * 4096 + kitem);
         const uint32_t d_s = tmem + t * 128;
         const uint32_t qa = q_base + t * Cfg::kQBytes;
         const uint32_t kb = slot_addr(kitem);
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_commit(&bars->s_full[t]);
       };
       auto issue_pv = [&](int t, int vitem, int j) {
+        trace(p.trace, p.trace_cta, 3, t * 4096 + j);
         const uint32_t d_o = tmem + 256 + t * D;
         const uint32_t a_p = tmem + t * 128;
         const uint32_t vb = slot_addr(vitem);
@@ -284,6 +287,7 @@ __global__ void __launch_bounds__(384, 1)
       float x[128];
       mbar_wait(&bars->s_full[t], j & 1);
       tc_fence_after();
+      if (r == 0) trace(p.trace, p.trace_cta, 10, t * 4096 + j);
       {
         uint32_t* xr = reinterpret_cast<uint32_t*>(x);
         tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(xr + 0));
@@ -370,6 +374,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
+      if (r == 0) trace(p.trace, p.trace_cta, 11, t * 4096 + j);
       if (lane == 0) mbar_arrive(&bars->p_ready[t]);
     }
 

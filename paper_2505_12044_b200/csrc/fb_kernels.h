@@ -20,6 +20,7 @@ struct FwdParams {
   int uq_bb, uq_hb;   // factor / bias broadcast flags (size-1 dims)
   int uk_bb, uk_hb;
   int bias_bb, bias_hb;
+  unsigned long long* trace; int trace_cta;  // FB_TRACE builds only
 };
 
 struct FwdMaps {
@@ -43,6 +44,7 @@ struct BwdParams {
   float* duq; int64_t duq_sb, duq_sh, duq_sn;  // nullable, fp32 [B,H,N,Rpad]
   float* duk; int64_t duk_sb, duk_sh, duk_sn;
   int uq_bb, uq_hb, uk_bb, uk_hb, bias_bb, bias_hb;
+  unsigned long long* trace; int trace_cta;  // FB_TRACE builds only
 };
 
 struct BwdMaps {
@@ -97,6 +99,9 @@ cudaError_t launch_bwd_preprocess(const Tensor4& o, const Tensor4& dout, const T
                                   cudaStream_t s);
 
 int factor_pairs(int split);
+
+// debug timeline trace target (fb_debug_set_trace)
+void trace_target(unsigned long long** buf, int* cta);
 
 // launch accounting (fb_launch_count)
 void note_launch(int n = 1);

@@ -70,6 +70,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- timeline trace
+// Compiled in only with -DFB_TRACE=1 (the libflashbias_b200_trace.so build):
+// selected roles of one CTA append (event, SM clock) records to a device
+// buffer that fb_trace_read() copies out.  Zero cost in the product build.
+#ifndef FB_TRACE
+#define FB_TRACE 0
+#endif
+// buf[0] is the record counter; records follow.  Set via fb_debug_set_trace().
+__device__ __forceinline__ void trace(unsigned long long* buf, int cta, int ev, int a) {
+#if FB_TRACE
+  if (buf == nullptr || static_cast<int>(blockIdx.x) != cta) return;
+  const unsigned long long i = atomicAdd(buf, 1ull) + 1;
+  if (i < (1ull << 16))
+    buf[i] = (static_cast<unsigned long long>(ev & 0xff) << 56) | (static_cast<unsigned long long>(a & 0xffff) << 40) |
+             (static_cast<unsigned long long>(clock64()) & 0xffffffffffull);
+#else
+  (void)buf; (void)cta; (void)ev; (void)a;
+#endif
+}
+
 // ---------------------------------------------------------------- register budget
 template <uint32_t kRegs>
 __device__ __forceinline__ void regs_inc() {
