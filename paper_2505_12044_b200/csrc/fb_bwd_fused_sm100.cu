@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(384, 1)
         const int q0 = (i_start + c) * 64;
         const int slot = c % Cfg::kSlots, use = c / Cfg::kSlots;
         if (use > 0) mbar_wait(&bars->slot_empty[slot], (use - 1) & 1);
-        trace(p.trace, p.trace_cta, 60, c);
+        trace(p.trace, p.trace_cta, 21, c);
         uint8_t* dst = smem + Cfg::kRes + slot * Cfg::kSlot;
         uint64_t* fb_ = &bars->slot_full[slot];
         mbar_arrive_expect_tx(fb_, Cfg::kItem);
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t qb = slot_addr(c), dob = qb + Cfg::kTile64;
         mbar_wait(&bars->p_ready, c & 1);
         tc_fence_after();
-        trace(p.trace, p.trace_cta, 30, c);
+        trace(p.trace, p.trace_cta, 10, c);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO  (K = 64 queries)
           mma_ts(tmem + T_DV, tmem + T_ST + kk * 8, mnmajor_desc(dob, 64, 128, kk * 16), id_d,
@@ -211,12 +211,12 @@ __global__ void __launch_bounds__(384, 1)
         if (c + 1 < nblk) {
           wait_slot(c + 1);
           tc_fence_after();
-          trace(p.trace, p.trace_cta, 31, c + 1);
+          trace(p.trace, p.trace_cta, 11, c + 1);
           issue_st(c + 1);
         }
         mbar_wait(&bars->ds_ready, c & 1);
         tc_fence_after();
-        trace(p.trace, p.trace_cta, 32, c);
+        trace(p.trace, p.trace_cta, 12, c);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q
           mma_ts(tmem + T_DK, tmem + T_DPT + kk * 8, mnmajor_desc(qb, 64, 128, kk * 16), id_d,
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(384, 1)
         const int qbuf = c & 1, quse = c >> 1;
         if (quse > 0) mbar_wait(&bars->dq_free[qbuf], (quse - 1) & 1);
         tc_fence_after();
-        trace(p.trace, p.trace_cta, 33, c);
+        trace(p.trace, p.trace_cta, 13, c);
         const uint32_t dsb = smem_u32(ds_buf) + qbuf * Cfg::kDsBuf;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 keys)
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_commit(&bars->dq_full[qbuf]);
         tc_commit(&bars->dsbuf_free[qbuf]);
         if (c + 1 < nblk) {
-          trace(p.trace, p.trace_cta, 34, c + 1);
+          trace(p.trace, p.trace_cta, 14, c + 1);
           issue_dpt(c + 1);
         }
       }
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(384, 1)
       float pr[64];
       mbar_wait(&bars->st_full, c & 1);
       tc_fence_after();
-      if (r == 0) trace(p.trace, p.trace_cta, 40, c);
+      if (r == 0) trace(p.trace, p.trace_cta, 15, c);
       {
         uint32_t u[64];
         tmem_ld32(tmem + lane_off + T_ST, *reinterpret_cast<uint32_t(*)[32]>(u));
@@ -299,11 +299,11 @@ __global__ void __launch_bounds__(384, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (r == 0) trace(p.trace, p.trace_cta, 41, c);
+      if (r == 0) trace(p.trace, p.trace_cta, 16, c);
       if (lane == 0) mbar_arrive(&bars->p_ready);
       mbar_wait(&bars->dpt_full, c & 1);
       tc_fence_after();
-      if (r == 0) trace(p.trace, p.trace_cta, 42, c);
+      if (r == 0) trace(p.trace, p.trace_cta, 17, c);
       uint32_t pk[32];
       {
         uint32_t u[64];
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (r == 0) trace(p.trace, p.trace_cta, 43, c);
+      if (r == 0) trace(p.trace, p.trace_cta, 18, c);
       if (lane == 0) mbar_arrive(&bars->ds_ready);
     }
     // ---- epilogue: dV, dK rows
@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(384, 1)
       const int qbuf = c & 1, quse = c >> 1;
       mbar_wait(&bars->dq_full[qbuf], quse & 1);
       tc_fence_after();
-      if (leader) trace(p.trace, p.trace_cta, 50, c);
+      if (leader) trace(p.trace, p.trace_cta, 19, c);
       uint32_t u[64];
       tmem_ld32(tmem + lane_off + T_DQ + qbuf * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
       tmem_ld32(tmem + lane_off + T_DQ + qbuf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(384, 1)
       if (leader) {
         tma_reduce_add_4d(&tm_dqacc, dq_stage, 0, q0, h, b);
         bulk_commit();
-        trace(p.trace, p.trace_cta, 51, c);
+        trace(p.trace, p.trace_cta, 20, c);
       }
     }
     if (leader) bulk_wait0();

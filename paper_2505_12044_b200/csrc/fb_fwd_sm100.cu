@@ -133,9 +133,14 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
 
-  // item bookkeeping shared by all roles: step j holds K, [B0 if j<n0], B1, V (dense)
-  // or K, V (otherwise).  Only the last step of tile 0 can be missing.
-  auto step_base = [&](int j) { return j <= n0 ? j * Cfg::kIPS : n0 * Cfg::kIPS + (j - n0) * (Cfg::kIPS - 1); };
+  // KV blocks are visited in REVERSE order (step s -> block j = n1-1-s): for a
+  // causal ALiBi-style bias the diagonal block holds the row max, so the lazy
+  // rescale almost never fires afterwards.  Tile 1 can own one more block than
+  // tile 0 (causal); tile 0 joins at step d = n1 - n0.
+  // Ring items of step s: K, [B0 if s >= d], B1, V (dense) or K, V.
+  const int dlt = n1 - n0;
+  auto step_base = [&](int st) { return DENSE ? st * Cfg::kIPS - min(st, dlt) : st * Cfg::kIPS; };
+  auto step_items = [&](int st) { return (DENSE && st < dlt) ? Cfg::kIPS - 1 : Cfg::kIPS; };
 
   if (warp >= 8) {
   regs_dec<80>();
@@ -155,14 +160,14 @@ __global__ void __launch_bounds__(384, 1)
                       &bars->q_full, pn * 16, row0 + t * kTileRows, hq, bq);
       }
       int item = 0;
-      for (int j = 0; j < n1; ++j) {
-        const int kv0 = j * kTileRows;
-        const int npos = (DENSE && j >= n0) ? Cfg::kIPS - 1 : Cfg::kIPS;
+      for (int st = 0; st < n1; ++st) {
+        const int kv0 = (n1 - 1 - st) * kTileRows;
+        const int npos = step_items(st);
         for (int pos = 0; pos < npos; ++pos, ++item) {
           const int slot = item % Cfg::kSlots;
           const int use = item / Cfg::kSlots;
           if (use > 0) mbar_wait(&bars->slot_empty[slot], (use - 1) & 1);
-          trace(p.trace, p.trace_cta, 20, item);
+          trace(p.trace, p.trace_cta, 4, item);
           uint8_t* dst = smem + Cfg::kQRegion + slot * Cfg::kSlotBytes;
           uint64_t* fb_ = &bars->slot_full[slot];
           if (pos == 0) {  // K (+ fk panels)
@@ -193,17 +198,18 @@ __global__ void __launch_bounds__(384, 1)
       auto slot_addr = [&](int item) { return ring_base + (item % Cfg::kSlots) * Cfg::kSlotBytes; };
       auto wait_full = [&](int item) {
         mbar_wait(&bars->slot_full[item % Cfg::kSlots], (item / Cfg::kSlots) & 1);
+        tc_fence_after();
       };
       auto release = [&](int item) {
         uint64_t* e = &bars->slot_empty[item % Cfg::kSlots];
         mbar_arrive_cnt(e, 3);
         tc_commit(e);
       };
-      auto issue_s = [&](int t, int kitem) {
-        trace(p.trace, p.trace_cta, 2, t * 4096 + kitem);
+      auto issue_s = [&](int t, int st) {
+        trace(p.trace, p.trace_cta, 2, t * 1024 + st);
         const uint32_t d_s = tmem + t * 128;
         const uint32_t qa = q_base + t * Cfg::kQBytes;
-        const uint32_t kb = slot_addr(kitem);
+        const uint32_t kb = slot_addr(step_base(st));
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           mma_ss(d_s, kmajor_desc(qa, kTileRows, Cfg::kSW, kk * 16),
@@ -214,55 +220,51 @@ __global__ void __launch_bounds__(384, 1)
                  make_sdesc(kb + Cfg::kQBytes + pn * Cfg::kPanelBytes, 16, 256, 6), idesc_qk, 1u);
         tc_commit(&bars->s_full[t]);
       };
-      auto issue_pv = [&](int t, int vitem, int j) {
-        trace(p.trace, p.trace_cta, 3, t * 4096 + j);
+      auto issue_pv = [&](int t, int vitem, bool acc) {
+        trace(p.trace, p.trace_cta, 3, t * 1024 + vitem);
         const uint32_t d_o = tmem + 256 + t * D;
         const uint32_t a_p = tmem + t * 128;
         const uint32_t vb = slot_addr(vitem);
 #pragma unroll
         for (int kk = 0; kk < kTileRows / 16; ++kk)
           mma_ts(d_o, a_p + kk * 8, mnmajor_desc(vb, kTileRows, Cfg::kSW, kk * 16), idesc_pv,
-                 (j > 0 || kk > 0) ? 1u : 0u);
+                 (acc || kk > 0) ? 1u : 0u);
       };
-      auto k_item = [&](int j) { return step_base(j); };
-      auto v_item = [&](int j) {
-        const int npos = (DENSE && j >= n0) ? Cfg::kIPS - 1 : Cfg::kIPS;
-        return step_base(j) + npos - 1;
-      };
+      auto v_item = [&](int st) { return step_base(st) + step_items(st) - 1; };
 
       mbar_wait(&bars->q_full, 0);
       tc_fence_after();
-      // prologue: S0(0), S1(0)
-      wait_full(k_item(0));
-      tc_fence_after();
-      if (n0 > 0) issue_s(0, k_item(0));
-      issue_s(1, k_item(0));
-      release(k_item(0));
-      for (int j = 0; j < n1; ++j) {
-        const int vi = v_item(j);
+      // prologue: tile 1's first S, and tile 0's first S (same step when d == 0)
+      wait_full(step_base(0));
+      if (dlt == 0) issue_s(0, 0);
+      issue_s(1, 0);
+      release(step_base(0));
+      if (dlt == 1 && n1 > 1) {
+        wait_full(step_base(1));
+        issue_s(0, 1);
+      }
+      for (int st = 0; st < n1; ++st) {
+        const int vi = v_item(st);
         wait_full(vi);
-        tc_fence_after();
-        if (j < n0) {
-          mbar_wait(&bars->p_ready[0], j & 1);
+        if (st >= dlt) {
+          mbar_wait(&bars->p_ready[0], (st - dlt) & 1);
           tc_fence_after();
-          issue_pv(0, vi, j);
-          if (j + 1 < n0) {
-            wait_full(k_item(j + 1));
-            tc_fence_after();
-            issue_s(0, k_item(j + 1));
+          issue_pv(0, vi, st > dlt);
+          if (st + 1 < n1) {
+            wait_full(step_base(st + 1));
+            issue_s(0, st + 1);
           } else {
             tc_commit(&bars->o_final[0]);
           }
         }
-        mbar_wait(&bars->p_ready[1], j & 1);
+        mbar_wait(&bars->p_ready[1], st & 1);
         tc_fence_after();
-        issue_pv(1, vi, j);
+        issue_pv(1, vi, st > 0);
         release(vi);
-        if (j + 1 < n1) {
-          wait_full(k_item(j + 1));
-          tc_fence_after();
-          issue_s(1, k_item(j + 1));
-          release(k_item(j + 1));
+        if (st + 1 < n1) {
+          wait_full(step_base(st + 1));
+          issue_s(1, st + 1);
+          release(step_base(st + 1));
         } else {
           tc_commit(&bars->o_final[1]);
         }
@@ -282,12 +284,13 @@ __global__ void __launch_bounds__(384, 1)
     const float sl2 = p.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
 
-    for (int j = 0; j < n_t; ++j) {
-      const int kv0 = j * kTileRows;
+    for (int it = 0; it < n_t; ++it) {
+      const int st = it + (t == 0 ? dlt : 0);  // global step
+      const int kv0 = (n1 - 1 - st) * kTileRows;
       float x[128];
-      mbar_wait(&bars->s_full[t], j & 1);
+      mbar_wait(&bars->s_full[t], it & 1);
       tc_fence_after();
-      if (r == 0) trace(p.trace, p.trace_cta, 10, t * 4096 + j);
+      if (r == 0) trace(p.trace, p.trace_cta, 5, t * 1024 + it);
       {
         uint32_t* xr = reinterpret_cast<uint32_t*>(x);
         tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(xr + 0));
@@ -296,9 +299,9 @@ __global__ void __launch_bounds__(384, 1)
         tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(xr + 96));
         tmem_wait_ld();
       }
+      // x holds raw Q'K'^T (DENSE: already scaled to log2 units with the bias added)
       if constexpr (DENSE) {
-        // this tile's bias item for step j
-        const int item = step_base(j) + 1 + (t == 1 && j < n0 ? 1 : 0);
+        const int item = step_base(st) + 1 + (t == 1 && st >= dlt ? 1 : 0);
         const int slot = item % Cfg::kSlots;
         mbar_wait(&bars->slot_full[slot], (item / Cfg::kSlots) & 1);
         const uint8_t* bt = smem + Cfg::kQRegion + slot * Cfg::kSlotBytes;
@@ -313,15 +316,14 @@ __global__ void __launch_bounds__(384, 1)
           for (int e = 0; e < 4; ++e) {
             const float2 bb = unpack2<BF16>(w[e]);
             const int c = c8 * 8 + e * 2;
-            x[c] = fmaf(x[c], sl2, bb.x * kLog2e);
-            x[c + 1] = fmaf(x[c + 1], sl2, bb.y * kLog2e);
+            const float2 r2 = ffma2(make_float2(x[c], x[c + 1]), make_float2(sl2, sl2),
+                                    make_float2(bb.x * kLog2e, bb.y * kLog2e));
+            x[c] = r2.x;
+            x[c + 1] = r2.y;
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars->slot_empty[slot]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 128; ++c) x[c] *= sl2;
       }
       const bool edge = (kv0 + kTileRows > p.M) || (p.causal && kv0 + kTileRows > row0 + t * kTileRows);
       if (edge) {
@@ -331,35 +333,50 @@ __global__ void __launch_bounds__(384, 1)
           if (col >= p.M || (p.causal && col > row)) x[c] = -INFINITY;
         }
       }
-      float mx = x[0];
+      // row max: a 3-input max tree over independent partials
+      float mx;
+      {
+        float m4[4];
 #pragma unroll
-      for (int c = 1; c < 128; ++c) mx = fmaxf(mx, x[c]);
-      const float m_new = fmaxf(m_run, mx);
+        for (int g = 0; g < 4; ++g) {
+          float a = x[32 * g];
+#pragma unroll
+          for (int c = 1; c < 31; c += 2) a = fmax3(a, x[32 * g + c], x[32 * g + c + 1]);
+          m4[g] = fmaxf(a, x[32 * g + 31]);
+        }
+        mx = fmax3(fmaxf(m4[0], m4[1]), m4[2], m4[3]);
+      }
+      const float m_new = DENSE ? fmaxf(m_run, mx) : fmaxf(m_run, mx * sl2);
       // lazy rescale: move the running max only when it grows by > 8 (log2 units)
       bool need = false;
       float alpha = 1.0f;
-      if (j == 0) {
+      if (it == 0) {
         m_run = m_new;
       } else if (m_new > m_run + 8.0f) {
         need = true;
         alpha = ex2(m_run - m_new);
         m_run = m_new;
       }
-      float sum = 0.f;
+      // p = 2^(x*sl2 - m): packed FFMA2, MUFU ex2, packed FADD2 partial sums
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       {
+        const float2 mul = DENSE ? make_float2(1.f, 1.f) : make_float2(sl2, sl2);
+        const float2 neg = make_float2(-m_run, -m_run);
         uint32_t pk[64];
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
-          const float p0 = ex2(x[2 * c] - m_run);
-          const float p1 = ex2(x[2 * c + 1] - m_run);
-          sum += p0 + p1;
-          pk[c] = pack2<BF16>(p0, p1);
+          const float2 e2 = ffma2(make_float2(x[2 * c], x[2 * c + 1]), mul, neg);
+          const float2 p2 = make_float2(ex2(e2.x), ex2(e2.y));
+          acc[c & 3] = fadd2(acc[c & 3], p2);
+          pk[c] = pack2<BF16>(p2.x, p2.y);
         }
         tmem_st32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(pk + 0));
         tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32));
       }
-      l_run = l_run * alpha + sum;
-      // O_t was last written by PV_t(j-1), which completed before S_t(j) (commit order)
+      const float2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+      const float2 s4 = fadd2(s01, s23);
+      l_run = l_run * alpha + (s4.x + s4.y);
+      // O_t was last written by PV_t(previous), which completed before S_t(this) (commit order)
       if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 32) {
@@ -367,14 +384,20 @@ __global__ void __launch_bounds__(384, 1)
           tmem_ld32(t_o + c0, o);
           tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          for (int c = 0; c < 32; c += 2) {
+            const float2 v2 = fmul2(make_float2(__uint_as_float(o[c]), __uint_as_float(o[c + 1])),
+                                    make_float2(alpha, alpha));
+            o[c] = __float_as_uint(v2.x);
+            o[c + 1] = __float_as_uint(v2.y);
+          }
           tmem_st32(t_o + c0, o);
         }
       }
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (r == 0) trace(p.trace, p.trace_cta, 11, t * 4096 + j);
+      if (r == 0) trace(p.trace, p.trace_cta, 6, t * 1024 + it);
+      if (lane == 0) trace(p.trace, p.trace_cta, 22 + (warp & 3), t * 1024 + it);
       if (lane == 0) mbar_arrive(&bars->p_ready[t]);
     }
 

@@ -77,14 +77,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #ifndef FB_TRACE
 #define FB_TRACE 0
 #endif
-// buf[0] is the record counter; records follow.  Set via fb_debug_set_trace().
+// Records are written to fixed slots buf[ev * 2048 + (a & 2047)] (ev < 32) with
+// plain stores — no atomics, so tracing barely perturbs the timeline.
 __device__ __forceinline__ void trace(unsigned long long* buf, int cta, int ev, int a) {
 #if FB_TRACE
   if (buf == nullptr || static_cast<int>(blockIdx.x) != cta) return;
-  const unsigned long long i = atomicAdd(buf, 1ull) + 1;
-  if (i < (1ull << 16))
-    buf[i] = (static_cast<unsigned long long>(ev & 0xff) << 56) | (static_cast<unsigned long long>(a & 0xffff) << 40) |
-             (static_cast<unsigned long long>(clock64()) & 0xffffffffffull);
+  buf[(ev & 31) * 2048 + (a & 2047)] = static_cast<unsigned long long>(clock64());
 #else
   (void)buf; (void)cta; (void)ev; (void)a;
 #endif
@@ -272,6 +270,37 @@ __device__ __forceinline__ uint64_t mnmajor_desc(uint32_t tile_base, int rows, i
 }
 
 // ---------------------------------------------------------------- math
+// packed fp32x2 (FFMA2 / FADD2 / FMUL2 on sm_100a): two lanes of work per instruction
+__device__ __forceinline__ uint64_t f2_as_u64(float2 v) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 u64_as_f2(uint64_t u) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(u));
+  return v;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
+  return u64_as_f2(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(r);
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
