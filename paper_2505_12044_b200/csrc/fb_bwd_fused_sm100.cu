@@ -4,19 +4,28 @@
 // Same math as fb_bwd_sm100.cu (oracle/flashbias_oracle.py:attention_bwd):
 //   S^T = K' Q'^T, P^T = exp(scale S^T - lse), dP^T = V dO^T,
 //   dS^T = P^T (dP^T - D), dV += P^T dO, dK += dS^T Q, dQ += scale dS K.
-// CTA owns 128 key rows and streams 64-row query blocks (causal: only the
+// CTA owns 128 key rows and streams 64-row query blocks c (causal: only the
 // blocks at or below the diagonal).  dQ is produced transposed on the tensor
-// core as dQ^T = K^T dS^T (M = d = 128, N = 64 queries), so it fits next to
-// the dK / dV accumulators in TMEM; each 64x128 fp32 dQ tile is staged in
-// shared memory and added into an fp32 accumulator in global memory with
-// one TMA bulk reduction (cp.reduce.async.bulk.tensor .add) — the per-head
-// accumulator (8 MB at N=16k) stays L2-resident under head-major scheduling.
+// core as dQ^T = K^T dS^T (M = d = 128, N = 64 queries); each 64x128 fp32 dQ
+// tile is staged in shared memory and added into an fp32 accumulator in
+// global memory with one TMA bulk reduction (cp.reduce.async.bulk.tensor
+// .add) — the per-head accumulator (8 MB at N=16k) stays L2-resident under
+// head-major scheduling.
 //
-// Warp roles (384 threads, 3 warpgroups for setmaxnreg):
-//   warps 0-3  elementwise: thread = key row = TMEM lane (P^T, dS^T)
-//   warps 4-7  dQ drain: thread = head-dim lane of dQ^T, TMEM -> smem -> TMA reduce
-//   warp  8    TMA producer, warp 9 TMEM alloc + MMA issuer, warps 10-11 idle
-// TMEM: S^T [0,64) dP^T [64,128) dV [128,256) dK [256,384) dQ^T_b [384+64b, +64)
+// Two elementwise warpgroups ping-pong over the query blocks (EW0: even c,
+// EW1: odd c) so the softmax-like work of one block overlaps the tensor-core
+// work of the other.  TMEM (512 columns):
+//   S^T_x [64x, 64x+64)   dP^T_x / dQ^T_x [128+64x, +64)   dV [256,384)   dK [384,512)
+// P^T and dS^T (bf16) are written over the first 32 columns of their fp32
+// source and consumed from TMEM as the A operand of dV / dK; dQ^T(c) reuses
+// the dP^T_x columns once dK(c) has been issued (tcgen05 MMAs run in order).
+// MMA order per block c (x = c & 1):
+//   dV(c) | dP^T(c+1) | dK(c) dQ^T(c) | S^T(c+2)
+//
+// Warp roles (512 threads, 4 warpgroups for setmaxnreg):
+//   warps 0-3 EW0, 4-7 EW1 (thread = key row = TMEM lane), 8-11 dQ drain
+//   (thread = head-dim lane of dQ^T: TMEM -> smem -> TMA reduce), warp 12 TMA
+//   producer, warp 13 TMEM alloc + MMA issuer, 14-15 idle.
 #include "fb_kernels.h"
 #include "fb_sm100.cuh"
 
@@ -41,17 +50,16 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 template <int RP, bool DENSE>
 struct FusedCfg {
   static constexpr int D = 128;
-  static constexpr int kSW = 128;
   static constexpr int kTile128 = 128 * D * 2;  // 32 KB
   static constexpr int kTile64 = 64 * D * 2;    // 16 KB
   static constexpr int kPanel128 = 128 * 32;
   static constexpr int kPanel64 = 64 * 32;
-  static constexpr int kRes = 2 * kTile128 + RP * kPanel128;                                  // K, V, Uk
-  static constexpr int kItem = 2 * kTile64 + (DENSE ? 64 * 128 * 2 : RP * kPanel64);       // Q, dO, Uq | bias^T
+  static constexpr int kRes = 2 * kTile128 + RP * kPanel128;                             // K, V, Uk
+  static constexpr int kItem = 2 * kTile64 + (DENSE ? 64 * 128 * 2 : RP * kPanel64);  // Q, dO, Uq | bias^T
   static constexpr int kSlot = (kItem + 1023) / 1024 * 1024;
-  static constexpr int kDsBuf = 128 * 128;  // dS^T [128 keys][64 queries] bf16, SW128
-  static constexpr int kDqStage = 64 * D * 4;  // 32 KB fp32
-  static constexpr int kMisc = 1024 + 512;     // stats + barriers
+  static constexpr int kDsBuf = 128 * 128;     // dS^T [128 keys][64 queries] bf16, SW128
+  static constexpr int kDqStage = 32 * D * 4;  // 16 KB fp32: a dQ tile drains in two 32-query halves
+  static constexpr int kMisc = 2048 + 512;     // stats [2 groups][2][128] + barriers
   static constexpr int kBudget = 232448 - 1024;
   static constexpr int kSlotsFit = (kBudget - kRes - 2 * kDsBuf - kDqStage - kMisc) / kSlot;
   static constexpr int kSlots = kSlotsFit > 4 ? 4 : kSlotsFit;
@@ -60,14 +68,15 @@ struct FusedCfg {
 };
 
 struct FusedBars {
-  uint64_t res_full, st_full, dpt_full, p_ready, ds_ready, final_;
+  uint64_t res_full, final_[2];
+  uint64_t st_full[2], dpt_full[2], p_ready[2], ds_ready[2];
   uint64_t dq_full[2], dq_free[2], dsbuf_free[2];
   uint64_t slot_full[4], slot_empty[4];
   uint32_t tmem_base;
 };
 
 template <int RP, bool DENSE, bool BF16>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(512, 1)
     fb_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                         const __grid_constant__ CUtensorMap tm_uq, const __grid_constant__ CUtensorMap tm_biasT,
                         const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -83,8 +92,8 @@ __global__ void __launch_bounds__(384, 1)
   const uint32_t ring_base = sbase + Cfg::kRes;
   uint8_t* ds_buf = smem + Cfg::kRes + Cfg::kSlots * Cfg::kSlot;  // 2 x 16 KB
   float* dq_stage = reinterpret_cast<float*>(ds_buf + 2 * Cfg::kDsBuf);
-  float* s_stats = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(dq_stage) + Cfg::kDqStage);  // [2][128]
-  FusedBars* bars = reinterpret_cast<FusedBars*>(reinterpret_cast<uint8_t*>(s_stats) + 1024);
+  float* s_stats = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(dq_stage) + Cfg::kDqStage);  // [2][2][128]
+  FusedBars* bars = reinterpret_cast<FusedBars*>(reinterpret_cast<uint8_t*>(s_stats) + 2048);
 
   const int warp = warp_id(), lane = lane_id();
   const int nkt = (p.M + 127) / 128;
@@ -96,7 +105,7 @@ __global__ void __launch_bounds__(384, 1)
   const int i_start = p.causal ? kv0 / 64 : 0;
   const int nblk = nqb - i_start;
 
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_k);
@@ -108,12 +117,13 @@ __global__ void __launch_bounds__(384, 1)
     }
     if (DENSE) tma_prefetch(&tm_biasT);
     mbar_init(&bars->res_full, 1);
-    mbar_init(&bars->st_full, 1);
-    mbar_init(&bars->dpt_full, 1);
-    mbar_init(&bars->p_ready, 4);
-    mbar_init(&bars->ds_ready, 4);
-    mbar_init(&bars->final_, 1);
+    mbar_init(&bars->final_[0], 1);
+    mbar_init(&bars->final_[1], 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars->st_full[i], 1);
+      mbar_init(&bars->dpt_full[i], 1);
+      mbar_init(&bars->p_ready[i], 4);
+      mbar_init(&bars->ds_ready[i], 4);
       mbar_init(&bars->dq_full[i], 1);
       mbar_init(&bars->dq_free[i], 4);
       mbar_init(&bars->dsbuf_free[i], 1);
@@ -124,16 +134,16 @@ __global__ void __launch_bounds__(384, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(&bars->tmem_base);
+  if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  constexpr uint32_t T_ST = 0, T_DPT = 64, T_DV = 128, T_DK = 256, T_DQ = 384;
+  constexpr uint32_t T_ST = 0, T_DPT = 128, T_DV = 256, T_DK = 384;
 
-  if (warp >= 8) {
+  if (warp >= 12) {
     regs_dec<96>();
-    if (warp == 8 && lane == 0) {
+    if (warp == 12 && lane == 0) {
       // ------------------------------------------------------------ TMA producer
       const int hq = p.uq_hb ? 0 : h, bq = p.uq_bb ? 0 : b;
       const int hk = p.uk_hb ? 0 : h, bk = p.uk_bb ? 0 : b;
@@ -165,109 +175,142 @@ __global__ void __launch_bounds__(384, 1)
             tma_load_4d(dst + 2 * Cfg::kTile64 + pn * Cfg::kPanel64, &tm_uq, fb_, pn * 16, q0, hq, bq);
         }
       }
-    } else if (warp == 9 && lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t id_s = make_idesc(128, 64, false, false, BF16);    // S^T, dP^T
-      constexpr uint32_t id_d = make_idesc(128, D, false, true, BF16);      // dV, dK (A from TMEM)
-      constexpr uint32_t id_q = make_idesc(128, 64, true, true, BF16);      // dQ^T = K^T dS^T
+    } else if ((warp == 13 || warp == 14) && lane == 0) {
+      // ------------------------------------------------------------ MMA issuers
+      // Two issuing threads, one per elementwise group x: each runs the chain of
+      // its own blocks c = x, x+2, ... so a stall on one group never holds back
+      // the other's tensor-core work (dV/dK accumulate from both; they are
+      // zero-initialised by EW0 and every MMA into them accumulates).
+      const int x = warp - 13;
+      constexpr uint32_t id_s = make_idesc(128, 64, false, false, BF16);  // S^T, dP^T
+      constexpr uint32_t id_d = make_idesc(128, D, false, true, BF16);    // dV, dK (A from TMEM)
+      constexpr uint32_t id_q = make_idesc(128, 64, true, true, BF16);    // dQ^T = K^T dS^T
+      // loop-invariant descriptors; per-K-step variants are constant adds to the
+      // start-address field (addresses < 256 KB, so the 14-bit field never carries)
+      const uint64_t dk_k = kmajor_desc(k_base, 128, 128, 0);   // K as A (K-major)
+      const uint64_t dk_v = kmajor_desc(v_base, 128, 128, 0);   // V as A (K-major)
+      const uint64_t dk_kt = mnmajor_desc(k_base, 128, 128, 0); // K^T as A (MN-major)
+      const uint64_t dsb = mnmajor_desc(smem_u32(ds_buf) + x * Cfg::kDsBuf, 128, 128, 0);
+      const uint32_t t_st = tmem + T_ST + 64 * x, t_dpt = tmem + T_DPT + 64 * x;
       auto slot_addr = [&](int c) { return ring_base + (c % Cfg::kSlots) * Cfg::kSlot; };
-      auto wait_slot = [&](int c) { mbar_wait(&bars->slot_full[c % Cfg::kSlots], (c / Cfg::kSlots) & 1); };
+      auto kstep = [](int kk) -> uint64_t { return (kk >> 2) * (64 * 128 >> 4) + (kk & 3) * 2; };  // 64-row tile
+      auto kstep128 = [](int kk) -> uint64_t { return (kk >> 2) * (128 * 128 >> 4) + (kk & 3) * 2; };
+      auto wait_slot = [&](int c) {
+        mbar_wait(&bars->slot_full[c % Cfg::kSlots], (c / Cfg::kSlots) & 1);
+        tc_fence_after();
+      };
       auto issue_st = [&](int c) {
         const uint32_t qb = slot_addr(c);
+        const uint64_t dq = kmajor_desc(qb, 64, 128, 0);
+        trace(p.trace, p.trace_cta, 11, c);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + T_ST, kmajor_desc(k_base, 128, 128, kk * 16), kmajor_desc(qb, 64, 128, kk * 16), id_s,
-                 kk > 0 ? 1u : 0u);
+          mma_ss(t_st, dk_k + kstep128(kk), dq + kstep(kk), id_s, kk > 0 ? 1u : 0u);
         if constexpr (!DENSE) {
 #pragma unroll
           for (int pn = 0; pn < RP; ++pn)
-            mma_ss(tmem + T_ST, make_sdesc(uk_base + pn * Cfg::kPanel128, 16, 256, 6),
+            mma_ss(t_st, make_sdesc(uk_base + pn * Cfg::kPanel128, 16, 256, 6),
                    make_sdesc(qb + 2 * Cfg::kTile64 + pn * Cfg::kPanel64, 16, 256, 6), id_s, 1u);
         }
-        tc_commit(&bars->st_full);
+        tc_commit(&bars->st_full[x]);
       };
       auto issue_dpt = [&](int c) {
-        const uint32_t dob = slot_addr(c) + Cfg::kTile64;
+        // dP^T_x last held dQ^T(c-2): wait for its drain
+        if (c >= 2) mbar_wait(&bars->dq_free[x], ((c >> 1) - 1) & 1);
+        tc_fence_after();
+        trace(p.trace, p.trace_cta, 14, c);
+        const uint64_t ddo = kmajor_desc(slot_addr(c) + Cfg::kTile64, 64, 128, 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + T_DPT, kmajor_desc(v_base, 128, 128, kk * 16), kmajor_desc(dob, 64, 128, kk * 16), id_s,
-                 kk > 0 ? 1u : 0u);
-        tc_commit(&bars->dpt_full);
+          mma_ss(t_dpt, dk_v + kstep128(kk), ddo + kstep(kk), id_s, kk > 0 ? 1u : 0u);
+        tc_commit(&bars->dpt_full[x]);
       };
       mbar_wait(&bars->res_full, 0);
-      wait_slot(0);
-      tc_fence_after();
-      issue_st(0);
-      issue_dpt(0);
-      for (int c = 0; c < nblk; ++c) {
-        const uint32_t qb = slot_addr(c), dob = qb + Cfg::kTile64;
-        mbar_wait(&bars->p_ready, c & 1);
+      if (x < nblk) {
+        wait_slot(x);
+        issue_st(x);
+        issue_dpt(x);
+      }
+      for (int c = x; c < nblk; c += 2) {
+        const int u = c >> 1;
+        const uint32_t qb = slot_addr(c);
+        const uint64_t mq = mnmajor_desc(qb, 64, 128, 0), mdo = mnmajor_desc(qb + Cfg::kTile64, 64, 128, 0);
+        mbar_wait(&bars->p_ready[x], u & 1);
         tc_fence_after();
         trace(p.trace, p.trace_cta, 10, c);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO  (K = 64 queries)
-          mma_ts(tmem + T_DV, tmem + T_ST + kk * 8, mnmajor_desc(dob, 64, 128, kk * 16), id_d,
-                 (c > 0 || kk > 0) ? 1u : 0u);
-        if (c + 1 < nblk) {
-          wait_slot(c + 1);
-          tc_fence_after();
-          trace(p.trace, p.trace_cta, 11, c + 1);
-          issue_st(c + 1);
-        }
-        mbar_wait(&bars->ds_ready, c & 1);
+          mma_ts(tmem + T_DV, t_st + kk * 8, mdo + kk * (16 * 128 >> 4), id_d, 1u);
+        mbar_wait(&bars->ds_ready[x], u & 1);
         tc_fence_after();
         trace(p.trace, p.trace_cta, 12, c);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q
-          mma_ts(tmem + T_DK, tmem + T_DPT + kk * 8, mnmajor_desc(qb, 64, 128, kk * 16), id_d,
-                 (c > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&bars->slot_empty[c % Cfg::kSlots]);
-        const int qbuf = c & 1, quse = c >> 1;
-        if (quse > 0) mbar_wait(&bars->dq_free[qbuf], (quse - 1) & 1);
-        tc_fence_after();
+          mma_ts(tmem + T_DK, t_dpt + kk * 8, mq + kk * (16 * 128 >> 4), id_d, 1u);
         trace(p.trace, p.trace_cta, 13, c);
-        const uint32_t dsb = smem_u32(ds_buf) + qbuf * Cfg::kDsBuf;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 keys)
-          mma_ss(tmem + T_DQ + qbuf * 64, mnmajor_desc(k_base, 128, 128, kk * 16),
-                 mnmajor_desc(dsb, 128, 128, kk * 16), id_q, kk > 0 ? 1u : 0u);
-        tc_commit(&bars->dq_full[qbuf]);
-        tc_commit(&bars->dsbuf_free[qbuf]);
-        if (c + 1 < nblk) {
-          trace(p.trace, p.trace_cta, 14, c + 1);
-          issue_dpt(c + 1);
+        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T (K = 128 keys), into the dP^T_x columns
+          mma_ss(t_dpt, dk_kt + kk * (16 * 128 >> 4), dsb + kk * (16 * 128 >> 4), id_q, kk > 0 ? 1u : 0u);
+        tc_commit(&bars->dq_full[x]);
+        tc_commit(&bars->dsbuf_free[x]);
+        tc_commit(&bars->slot_empty[c % Cfg::kSlots]);
+        if (c + 2 < nblk) {
+          wait_slot(c + 2);
+          issue_st(c + 2);
+          issue_dpt(c + 2);
         }
       }
-      tc_commit(&bars->final_);
+      tc_commit(&bars->final_[x]);
     }
-  } else if (warp < 4) {
-    regs_inc<224>();
+  } else if (warp < 8) {
+    regs_inc<160>();
     // -------------------------------------------------------------- elementwise (thread = key row)
-    const int r = threadIdx.x;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const int g = warp >> 2;          // EW group: blocks c with c % 2 == g
+    const int r = threadIdx.x & 127;  // key row within the tile == TMEM lane
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    const uint32_t t_st = tmem + lane_off + T_ST + 64 * g;
+    const uint32_t t_dpt = tmem + lane_off + T_DPT + 64 * g;
     const int kv = kv0 + r;
     const float* lse_g = p.lse + static_cast<int64_t>(b * p.H + h) * p.N;
     const float* dl_g = p.delta + static_cast<int64_t>(b * p.H + h) * p.N;
-    for (int c = 0; c < nblk; ++c) {
+    {  // zero the dV / dK accumulators (every MMA into them accumulates); each group clears one
+      uint32_t z[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) z[i] = 0u;
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) tmem_st32(tmem + lane_off + (g == 0 ? T_DV : T_DK) + c0, z);
+      tmem_wait_st();
+      tc_fence_before();
+    }
+    named_bar_sync(4, 256);  // both accumulators cleared before any EW arrival (MMAs wait on those)
+    tc_fence_after();
+    for (int c = g; c < nblk; c += 2) {
+      const int u = c >> 1;
       const int q0 = (i_start + c) * 64;
-      float* st = s_stats + (c & 1) * 128;
+      float* st = s_stats + (g * 2 + (u & 1)) * 128;
       {
         const int qq = r & 63, q = q0 + qq;
         if (r < 64) st[qq] = q < p.N ? lse_g[q] * kLog2eF : INFINITY;
         else st[64 + qq] = q < p.N ? dl_g[q] : 0.f;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + g, 128);
       float pr[64];
-      mbar_wait(&bars->st_full, c & 1);
+      mbar_wait(&bars->st_full[g], u & 1);
       tc_fence_after();
       if (r == 0) trace(p.trace, p.trace_cta, 15, c);
       {
-        uint32_t u[64];
-        tmem_ld32(tmem + lane_off + T_ST, *reinterpret_cast<uint32_t(*)[32]>(u));
-        tmem_ld32(tmem + lane_off + T_ST + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+        uint32_t v[64];
+        tmem_ld32(t_st, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(t_st + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_wait_ld();
+        const float2 mul = make_float2(p.scale_log2, p.scale_log2);
 #pragma unroll
-        for (int qq = 0; qq < 64; ++qq) pr[qq] = fmaf(__uint_as_float(u[qq]), p.scale_log2, -st[qq]);
+        for (int qq = 0; qq < 64; qq += 2) {
+          const float2 r2 = ffma2(make_float2(__uint_as_float(v[qq]), __uint_as_float(v[qq + 1])), mul,
+                                  make_float2(-st[qq], -st[qq + 1]));
+          pr[qq] = r2.x;
+          pr[qq + 1] = r2.y;
+        }
       }
       if constexpr (DENSE) {
         mbar_wait(&bars->slot_full[c % Cfg::kSlots], (c / Cfg::kSlots) & 1);
@@ -283,44 +326,48 @@ __global__ void __launch_bounds__(384, 1)
           pr[qq] = fmaf(bv, kLog2eF, pr[qq]);
         }
       }
-      const bool edge = p.causal && (q0 < kv0 + 128);
+      if (p.causal && (q0 < kv0 + 128)) {
 #pragma unroll
-      for (int qq = 0; qq < 64; ++qq) {
-        float x = pr[qq];
-        if (edge && kv > q0 + qq) x = -INFINITY;
-        pr[qq] = ex2(x);
+        for (int qq = 0; qq < 64; ++qq)
+          if (kv > q0 + qq) pr[qq] = -INFINITY;
       }
       {
         uint32_t pk[32];
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2) pk[c2] = pack2<BF16>(pr[2 * c2], pr[2 * c2 + 1]);
-        tmem_st32(tmem + lane_off + T_ST, pk);
+        for (int c2 = 0; c2 < 32; ++c2) {
+          pr[2 * c2] = ex2(pr[2 * c2]);
+          pr[2 * c2 + 1] = ex2(pr[2 * c2 + 1]);
+          pk[c2] = pack2<BF16>(pr[2 * c2], pr[2 * c2 + 1]);
+        }
+        tmem_st32(t_st, pk);
         tmem_wait_st();
       }
       tc_fence_before();
       __syncwarp();
       if (r == 0) trace(p.trace, p.trace_cta, 16, c);
-      if (lane == 0) mbar_arrive(&bars->p_ready);
-      mbar_wait(&bars->dpt_full, c & 1);
+      if (lane == 0) mbar_arrive(&bars->p_ready[g]);
+      mbar_wait(&bars->dpt_full[g], u & 1);
       tc_fence_after();
       if (r == 0) trace(p.trace, p.trace_cta, 17, c);
       uint32_t pk[32];
       {
-        uint32_t u[64];
-        tmem_ld32(tmem + lane_off + T_DPT, *reinterpret_cast<uint32_t(*)[32]>(u));
-        tmem_ld32(tmem + lane_off + T_DPT + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+        uint32_t v[64];
+        tmem_ld32(t_dpt, *reinterpret_cast<uint32_t(*)[32]>(v));
+        tmem_ld32(t_dpt + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
         tmem_wait_ld();
 #pragma unroll
-        for (int c2 = 0; c2 < 32; ++c2)
-          pk[c2] = pack2<BF16>(pr[2 * c2] * (__uint_as_float(u[2 * c2]) - st[64 + 2 * c2]),
-                               pr[2 * c2 + 1] * (__uint_as_float(u[2 * c2 + 1]) - st[64 + 2 * c2 + 1]));
+        for (int c2 = 0; c2 < 32; ++c2) {
+          const float2 dpd = fadd2(make_float2(__uint_as_float(v[2 * c2]), __uint_as_float(v[2 * c2 + 1])),
+                                   make_float2(-st[64 + 2 * c2], -st[64 + 2 * c2 + 1]));
+          const float2 ds = fmul2(make_float2(pr[2 * c2], pr[2 * c2 + 1]), dpd);
+          pk[c2] = pack2<BF16>(ds.x, ds.y);
+        }
       }
-      tmem_st32(tmem + lane_off + T_DPT, pk);
+      tmem_st32(t_dpt, pk);
       // dS^T row -> shared memory (B operand of dQ^T), SW128 MN-major: 16-byte
       // chunk ch of row r lives at chunk ch ^ (r & 7)
-      const int dbuf = c & 1;
-      if (c >= 2) mbar_wait(&bars->dsbuf_free[dbuf], ((c >> 1) - 1) & 1);
-      uint8_t* row = ds_buf + dbuf * Cfg::kDsBuf + r * 128;
+      if (u >= 1) mbar_wait(&bars->dsbuf_free[g], (u - 1) & 1);
+      uint8_t* row = ds_buf + g * Cfg::kDsBuf + r * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch)
         *reinterpret_cast<uint4*>(row + ((ch ^ (r & 7)) << 4)) =
@@ -330,79 +377,85 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_before();
       __syncwarp();
       if (r == 0) trace(p.trace, p.trace_cta, 18, c);
-      if (lane == 0) mbar_arrive(&bars->ds_ready);
+      if (lane == 0) mbar_arrive(&bars->ds_ready[g]);
     }
-    // ---- epilogue: dV, dK rows
-    mbar_wait(&bars->final_, 0);
-    tc_fence_after();
-    const bool valid = kv < p.M;
-    typedef typename std::conditional<BF16, __nv_bfloat16, __half>::type elem_t;
+    if (g == 0) {
+      // ---- epilogue (EW0): dV, dK rows, after both issuers' last MMAs
+      mbar_wait(&bars->final_[0], 0);
+      mbar_wait(&bars->final_[1], 0);
+      tc_fence_after();
+      const bool valid = kv < p.M;
+      typedef typename std::conditional<BF16, __nv_bfloat16, __half>::type elem_t;
 #pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem + lane_off + T_DV + c0, v);
-      tmem_wait_ld();
-      if (valid) {
-        elem_t* dst = reinterpret_cast<elem_t*>(p.dv) + static_cast<int64_t>(b) * p.dv_sb +
-                      static_cast<int64_t>(h) * p.dv_sh + static_cast<int64_t>(kv) * p.dv_sn + c0;
-        uint32_t o16[16];
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem + lane_off + T_DV + c0, v);
+        tmem_wait_ld();
+        if (valid) {
+          elem_t* dst = reinterpret_cast<elem_t*>(p.dv) + static_cast<int64_t>(b) * p.dv_sb +
+                        static_cast<int64_t>(h) * p.dv_sh + static_cast<int64_t>(kv) * p.dv_sn + c0;
+          uint32_t o16[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) o16[c] = pack2<BF16>(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
+          for (int c = 0; c < 16; ++c) o16[c] = pack2<BF16>(__uint_as_float(v[2 * c]), __uint_as_float(v[2 * c + 1]));
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          reinterpret_cast<uint4*>(dst)[q4] = make_uint4(o16[4 * q4], o16[4 * q4 + 1], o16[4 * q4 + 2], o16[4 * q4 + 3]);
-      }
-      tmem_ld32(tmem + lane_off + T_DK + c0, v);
-      tmem_wait_ld();
-      if (valid) {
-        elem_t* dst = reinterpret_cast<elem_t*>(p.dk) + static_cast<int64_t>(b) * p.dk_sb +
-                      static_cast<int64_t>(h) * p.dk_sh + static_cast<int64_t>(kv) * p.dk_sn + c0;
-        uint32_t o16[16];
+          for (int q4 = 0; q4 < 4; ++q4)
+            reinterpret_cast<uint4*>(dst)[q4] = make_uint4(o16[4 * q4], o16[4 * q4 + 1], o16[4 * q4 + 2], o16[4 * q4 + 3]);
+        }
+        tmem_ld32(tmem + lane_off + T_DK + c0, v);
+        tmem_wait_ld();
+        if (valid) {
+          elem_t* dst = reinterpret_cast<elem_t*>(p.dk) + static_cast<int64_t>(b) * p.dk_sb +
+                        static_cast<int64_t>(h) * p.dk_sh + static_cast<int64_t>(kv) * p.dk_sn + c0;
+          uint32_t o16[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          o16[c] = pack2<BF16>(__uint_as_float(v[2 * c]) * p.scale, __uint_as_float(v[2 * c + 1]) * p.scale);
+          for (int c = 0; c < 16; ++c)
+            o16[c] = pack2<BF16>(__uint_as_float(v[2 * c]) * p.scale, __uint_as_float(v[2 * c + 1]) * p.scale);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          reinterpret_cast<uint4*>(dst)[q4] = make_uint4(o16[4 * q4], o16[4 * q4 + 1], o16[4 * q4 + 2], o16[4 * q4 + 3]);
+          for (int q4 = 0; q4 < 4; ++q4)
+            reinterpret_cast<uint4*>(dst)[q4] = make_uint4(o16[4 * q4], o16[4 * q4 + 1], o16[4 * q4 + 2], o16[4 * q4 + 3]);
+        }
       }
     }
   } else {
-    regs_dec<128>();
-    // -------------------------------------------------------------- dQ drain (warps 4-7)
-    const int dd = threadIdx.x - 128;  // head-dim index = TMEM lane of dQ^T
+    regs_dec<96>();
+    // -------------------------------------------------------------- dQ drain (warps 8-11)
+    const int dd = threadIdx.x - 256;  // head-dim index = TMEM lane of dQ^T
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const bool leader = dd == 0;
     for (int c = 0; c < nblk; ++c) {
       const int q0 = (i_start + c) * 64;
-      const int qbuf = c & 1, quse = c >> 1;
-      mbar_wait(&bars->dq_full[qbuf], quse & 1);
+      const int x = c & 1, u = c >> 1;
+      mbar_wait(&bars->dq_full[x], u & 1);
       tc_fence_after();
       if (leader) trace(p.trace, p.trace_cta, 19, c);
-      uint32_t u[64];
-      tmem_ld32(tmem + lane_off + T_DQ + qbuf * 64, *reinterpret_cast<uint32_t(*)[32]>(u));
-      tmem_ld32(tmem + lane_off + T_DQ + qbuf * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(u + 32));
+      uint32_t v[64];
+      tmem_ld32(tmem + lane_off + T_DPT + 64 * x, *reinterpret_cast<uint32_t(*)[32]>(v));
+      tmem_ld32(tmem + lane_off + T_DPT + 64 * x + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->dq_free[qbuf]);
-      if (leader) bulk_wait_read0();  // previous reduction finished reading the stage
-      named_bar_sync(2, 128);
+      if (lane == 0) mbar_arrive(&bars->dq_free[x]);
 #pragma unroll
-      for (int qq = 0; qq < 64; ++qq) dq_stage[qq * D + dd] = __uint_as_float(u[qq]) * p.scale;
-      fence_proxy_async();
-      named_bar_sync(2, 128);
-      if (leader) {
-        tma_reduce_add_4d(&tm_dqacc, dq_stage, 0, q0, h, b);
-        bulk_commit();
-        trace(p.trace, p.trace_cta, 20, c);
+      for (int half = 0; half < 2; ++half) {
+        if (leader) bulk_wait_read0();  // previous reduction finished reading the stage
+        named_bar_sync(3, 128);
+#pragma unroll
+        for (int qq = 0; qq < 32; ++qq) dq_stage[qq * D + dd] = __uint_as_float(v[32 * half + qq]) * p.scale;
+        fence_proxy_async();
+        named_bar_sync(3, 128);
+        if (leader) {
+          tma_reduce_add_4d(&tm_dqacc, dq_stage, 0, q0 + 32 * half, h, b);
+          bulk_commit();
+        }
       }
+      if (leader) trace(p.trace, p.trace_cta, 20, c);
     }
     if (leader) bulk_wait0();
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -418,7 +471,7 @@ static cudaError_t launch_fused_t(const BwdMaps& m, const CUtensorMap& dqacc, co
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  k<<<((p.M + 127) / 128) * p.B * p.H, 384, Cfg::kSmem, s>>>(m.q64, m.do64, m.uq64, m.biasT, m.k128, m.v128,
+  k<<<((p.M + 127) / 128) * p.B * p.H, 512, Cfg::kSmem, s>>>(m.q64, m.do64, m.uq64, m.biasT, m.k128, m.v128,
                                                              m.uk128, dqacc, p);
   return cudaGetLastError();
 }

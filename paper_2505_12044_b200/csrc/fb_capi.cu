@@ -413,7 +413,7 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     tacc.stride[3] = 1; tacc.stride[2] = 128; tacc.stride[1] = (int64_t)N * 128; tacc.stride[0] = (int64_t)H * N * 128;
     tacc.dtype = FB_F32;
     CUtensorMap macc;
-    if ((rc = make_map(&macc, &tacc, 128, 64, 0, "dq_acc"))) return rc;
+    if ((rc = make_map(&macc, &tacc, 128, 32, 0, "dq_acc"))) return rc;
     e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * 128 * sizeof(float), s);
     if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
     e = launch_bwd_fused_sm100(rp, bias != nullptr, q->dtype == FB_BF16, maps, macc, p, s);

@@ -50,7 +50,7 @@ for t, e, a in fwd:
     d[a][e] = t
 sm = [v[6] - v[5] for v in d.values() if 5 in v and 6 in v]
 slow = [max(v.get(22 + w, 0) for w in range(4)) - v[5] for v in d.values() if 5 in v and 22 in v]
-print("fwd softmax per block (warp0):", sum(sm) / len(sm), " slowest warp:", sum(slow) / len(slow))
+print("fwd softmax per block (warp0):", sum(sm) / len(sm), " slowest warp:", sum(slow) / max(1, len(slow)))
 st = sorted(t for t, e, a in fwd if e == 5)
 print("fwd mean gap between softmax starts (alternating tiles):", (st[-1] - st[0]) / (len(st) - 1))
 mma = sorted(t for t, e, a in fwd if e in (2, 3))
@@ -60,9 +60,6 @@ for t, e, a in bwd:
     d[a][e] = t
 A = [v[16] - v[15] for v in d.values() if 15 in v and 16 in v]
 Bp = [v[18] - v[17] for v in d.values() if 17 in v and 18 in v]
-As = [max(v.get(22 + w, 0) for w in range(4)) - v[15] for v in d.values() if 15 in v and 22 in v]
-Bs = [max(v.get(26 + w, 0) for w in range(4)) - v[17] for v in d.values() if 17 in v and 26 in v]
-print("bwd phase A (w0)", sum(A) / len(A), "slowest", sum(As) / len(As), "| phase B (w0)", sum(Bp) / len(Bp),
-      "slowest", sum(Bs) / len(Bs))
+print("bwd phase A (w0)", sum(A) / len(A), "| phase B (w0)", sum(Bp) / len(Bp))
 a0 = sorted(t for t, e, a in bwd if e == 15)
 print("bwd block period", (a0[-1] - a0[0]) / (len(a0) - 1), "blocks", len(a0))
