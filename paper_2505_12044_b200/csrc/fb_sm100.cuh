@@ -307,6 +307,28 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
   return u64_as_f2(r);
 }
+// 2^x for a pair on the FMA/ALU pipes instead of MUFU (FA4-style offload):
+// Cody-Waite split x = r + f (r integer, |f| <= 1/2), 2^f by a degree-3
+// minimax polynomial (max relative error 7.5e-5, below bf16's 3.9e-3), r added
+// straight into the exponent field.  x < -127 (incl. -inf) returns 0.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = fadd2(xc, magic);                          // r in t's low mantissa bits
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), xc);
+  float2 p = ffma2(f, make_float2(0.055171619714035273f, 0.055171619714035273f),
+                   make_float2(0.2426111703820135f, 0.2426111703820135f));
+  p = ffma2(p, f, make_float2(0.6932609990852712f, 0.6932609990852712f));
+  p = ffma2(p, f, make_float2(0.9999280709467429f, 0.9999280709467429f));
+  const int ex0 = (__float_as_int(t.x) - 0x4B400000) << 23;
+  const int ex1 = (__float_as_int(t.y) - 0x4B400000) << 23;
+  float2 out;
+  out.x = x.x < -127.f ? 0.f : __int_as_float(__float_as_int(p.x) + ex0);
+  out.y = x.y < -127.f ? 0.f : __int_as_float(__float_as_int(p.y) + ex1);
+  return out;
+}
+
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
