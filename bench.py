@@ -197,11 +197,27 @@ def step_fn(cfg, inp, mode: str):
     return run
 
 
-def time_steps(fn, steps: int, warmup: int, dist=None):
+def time_steps(fn, steps: int, warmup: int, dist=None, graph: bool = False):
+    """CUDA-event timing of `steps` calls after `warmup` untimed ones, barrier +
+    synchronize on both sides.  graph=True captures one step in a CUDA graph
+    (after warm-up) and times its replays — for the microsecond-scale configs
+    whose step would otherwise be bound by Python launch overhead."""
     import torch
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn()
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        fn = g.replay
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -263,7 +279,11 @@ def run_gpu(args, cfg):
     device = torch.device("cuda", local)
     dist = None
     if world > 1:
-        dist_mod.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")  # gloo: functional test of >1 ranks on one GPU
+        if backend == "nccl":
+            dist_mod.init_process_group("nccl", device_id=device)
+        else:
+            dist_mod.init_process_group(backend)
         dist = dist_mod
     from paper_2505_12044_b200 import _lib
     lib = _lib.lib()
@@ -275,17 +295,36 @@ def run_gpu(args, cfg):
     n_loc = (hi - lo) * cfg["B"]
 
     fn = step_fn(cfg, inp, "flashbias")
+    use_graph = alg_flops(cfg, total_bh) < 20e9 and not args.no_graph
+    fn()  # one eager step: count this library's kernel launches per step
+    torch.cuda.synchronize()
     lib.fb_launch_count(1)
+    fn()
+    torch.cuda.synchronize()
+    launches_per_step = int(lib.fb_launch_count(1))
     with ClockSampler(local) as clk:
-        ms = time_steps(fn, args.steps, args.warmup, dist)
-    launches = int(lib.fb_launch_count(1))
-    launches_timed = launches * args.steps // (args.steps + args.warmup)
+        ms = time_steps(fn, args.steps, args.warmup, dist, graph=use_graph)
+    launches_timed = launches_per_step * args.steps
     if dist is not None:
         t = torch.tensor([ms], device=device)
         dist.all_reduce(t, op=dist_mod.ReduceOp.MAX)
         ms = float(t)
     flops = alg_flops(cfg, total_bh)
     tflops = flops / (ms * 1e-3) / 1e12
+    gather_ms = None
+    if dist is not None:  # NCCL all-gather of O and dQ/dK/dV after the kernels (outside the hot loop)
+        from paper_2505_12044_b200.sharding import gather_heads
+        outs = [inp["q"].detach()] * (4 if cfg["bwd"] else 1)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        ev0.record()
+        for t in outs:
+            gather_heads(t, cfg["H"])
+        ev1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([ev0.elapsed_time(ev1)], device=device)
+        dist.all_reduce(t, op=dist_mod.ReduceOp.MAX)
+        gather_ms = float(t)
 
     # dense-bias baseline on the same pipeline (same step, bias tensor [1,H_loc,N,N])
     dense_ms = None
@@ -302,7 +341,7 @@ def run_gpu(args, cfg):
                                                  _lib.ref(D(dense)), _lib.stream_ptr(device)))
         inp["dense"] = dense
         dfn = step_fn(cfg, inp, "dense")
-        dense_ms = time_steps(dfn, max(1, args.steps), max(1, min(args.warmup, 2)), dist)
+        dense_ms = time_steps(dfn, max(1, args.steps), max(1, min(args.warmup, 2)), dist, graph=use_graph)
         if dist is not None:
             t = torch.tensor([dense_ms], device=device)
             dist.all_reduce(t, op=dist_mod.ReduceOp.MAX)
@@ -349,11 +388,14 @@ def run_gpu(args, cfg):
                    "bwd": cfg["bwd"], "parallelism": f"bh-shard{world}",
                    "l2": "inputs larger than L2 (no flush needed)" if cfg["N"] * cfg["d"] * 2 * n_loc > 126e6
                    else "inputs smaller than L2 (repeated steps hit L2)"},
+        "gather_ms_per_step": None if gather_ms is None else round(gather_ms, 3),
+        "ms_per_step_with_gather": None if gather_ms is None else round(ms + gather_ms, 3),
         "dense_bias_ms_per_step": None if dense_ms is None else round(dense_ms, 3),
         "speedup_vs_dense_bias": None if dense_ms is None else round(dense_ms / ms, 3),
         "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches_timed,
+        "cuda_graph": use_graph,
         "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.skip_cpu:
@@ -515,6 +557,7 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-graph", action="store_true", help="never CUDA-graph the step (small configs use graphs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     cfg = CONFIGS[args.config]

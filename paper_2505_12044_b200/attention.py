@@ -142,6 +142,29 @@ def _padded_head_dim(c: int) -> int:
     raise ConfigError(f"head dim {c} > 128 is not supported by the sm_100a kernels")
 
 
+_SPLIT_CACHE: dict = {}
+
+
+def _split_key(fq, fk, premul, tol, max_cols):
+    """Identity of a factor pair for the split cache: storage, shape and the
+    in-place version counters (any write to the factors invalidates it)."""
+    def ident(t):
+        return (t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype, t._version)
+    return ident(fq), ident(fk), float(premul), float(tol), int(max_cols)
+
+
+def choose_split_cached(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int = 64) -> int:
+    """choose_split memoised per factor tensors (the decision needs a device->host
+    read; static factors such as ALiBi/spatial pay it once, not every call)."""
+    key = _split_key(fq, fk, premul, tol, max_cols)
+    k = _SPLIT_CACHE.get(key)
+    if k is None:
+        if len(_SPLIT_CACHE) > 256:
+            _SPLIT_CACHE.clear()
+        k = _SPLIT_CACHE[key] = choose_split(fq, fk, premul, tol, max_cols)
+    return k
+
+
 def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int = 64) -> int:
     """bf16 k-way split level for logical fp32 factors.
 
@@ -152,12 +175,14 @@ def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int =
     import torch
     a = fq.detach().float() * premul
     b = fk.detach().float()
-    if torch.equal(a.to(torch.bfloat16).float(), a) and torch.equal(b.to(torch.bfloat16).float(), b):
-        return 1
     r = a.shape[-1]
     amax = a.abs().amax(dim=tuple(range(a.dim() - 1)))
     bmax = b.abs().amax(dim=tuple(range(b.dim() - 1)))
-    scale = float((amax * bmax).sum())
+    inexact = ((a.to(torch.bfloat16).float() != a).any() | (b.to(torch.bfloat16).float() != b).any()).float()
+    stats = torch.stack([inexact, (amax * bmax).sum()]).cpu()  # one device->host read
+    if stats[0] == 0:
+        return 1
+    scale = float(stats[1])
     best = 1
     for k in (1, 2, 3):
         if r * k * (k + 1) // 2 > max_cols:
@@ -332,7 +357,7 @@ def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none",
                 bp = bt.contiguous()
         sp = None
         if fqt is not None:
-            sp = split or choose_split(fqt, fkt, premul, max_cols=64 if dp == 128 else 128)
+            sp = split or choose_split_cached(fqt, fkt, premul, max_cols=64 if dp == 128 else 128)
         o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(scale), float(premul), sp)
         o = o[..., : vt.shape[-1]]
     return _mirror(o, shp)
