@@ -275,6 +275,7 @@ def run_gpu(args, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("BENCH_FORCE_DEVICE", local))  # functional multi-rank test on one GPU
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     dist = None
