@@ -501,32 +501,33 @@ cudaError_t launch_bwd_fused_sm100(int rp, bool dense, bool bf16, const BwdMaps&
   return bf16 ? fused_rp<true>(rp, dense, m, dqacc, p, s) : fused_rp<false>(rp, dense, m, dqacc, p, s);
 }
 
-// dq[b,h,n,:] = dq_acc[b,h,n,:] (fp32 -> bf16/f16); the scale is applied in the drain
+// dq[b,h,n,:] = dq_acc[b,h,n,:] (fp32 [B,H,N,d] -> bf16/f16); the scale is applied in the drain
 template <bool BF16>
-__global__ void dq_convert_kernel(const float* __restrict__ acc, void* dq, int B, int H, int N, int64_t sb,
+__global__ void dq_convert_kernel(const float* __restrict__ acc, void* dq, int B, int H, int N, int d, int64_t sb,
                                   int64_t sh, int64_t sn) {
   typedef typename std::conditional<BF16, __nv_bfloat16, __half>::type elem_t;
   const int64_t rows = static_cast<int64_t>(B) * H * N;
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * 16;
+  const int per_row = d / 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < rows * per_row;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t row = i / 16, c8 = (i % 16) * 8;
+    const int64_t row = i / per_row, c8 = (i % per_row) * 8;
     const int64_t n = row % N, hh = (row / N) % H, bb = row / (static_cast<int64_t>(N) * H);
-    const float4 a = reinterpret_cast<const float4*>(acc + row * 128 + c8)[0];
-    const float4 c = reinterpret_cast<const float4*>(acc + row * 128 + c8)[1];
+    const float4 a = reinterpret_cast<const float4*>(acc + row * d + c8)[0];
+    const float4 c = reinterpret_cast<const float4*>(acc + row * d + c8)[1];
     elem_t* dst = reinterpret_cast<elem_t*>(dq) + bb * sb + hh * sh + n * sn + c8;
     *reinterpret_cast<uint4*>(dst) =
         make_uint4(pack2<BF16>(a.x, a.y), pack2<BF16>(a.z, a.w), pack2<BF16>(c.x, c.y), pack2<BF16>(c.z, c.w));
   }
 }
 
-cudaError_t launch_dq_convert(const float* acc, const BwdParams& p, bool bf16, cudaStream_t s) {
-  const int64_t work = static_cast<int64_t>(p.B) * p.H * p.N * 16;
+cudaError_t launch_dq_convert(const float* acc, int d, const BwdParams& p, bool bf16, cudaStream_t s) {
+  const int64_t work = static_cast<int64_t>(p.B) * p.H * p.N * (d / 8);
   int64_t g = (work + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
   if (bf16)
-    dq_convert_kernel<true><<<static_cast<int>(g), 256, 0, s>>>(acc, p.dq, p.B, p.H, p.N, p.dq_sb, p.dq_sh, p.dq_sn);
+    dq_convert_kernel<true><<<static_cast<int>(g), 256, 0, s>>>(acc, p.dq, p.B, p.H, p.N, d, p.dq_sb, p.dq_sh, p.dq_sn);
   else
-    dq_convert_kernel<false><<<static_cast<int>(g), 256, 0, s>>>(acc, p.dq, p.B, p.H, p.N, p.dq_sb, p.dq_sh, p.dq_sn);
+    dq_convert_kernel<false><<<static_cast<int>(g), 256, 0, s>>>(acc, p.dq, p.B, p.H, p.N, d, p.dq_sb, p.dq_sh, p.dq_sn);
   return cudaGetLastError();
 }
 

@@ -310,7 +310,7 @@ size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k) {
   if (!q) return 0;
   const size_t rows = (size_t)q->shape[0] * q->shape[1] * q->shape[2];
   size_t bytes = (rows * sizeof(float) + 255) / 256 * 256 + 256;  // delta
-  if (q->shape[3] == 128) bytes += rows * 128 * sizeof(float);    // fp32 dQ accumulator (fused path)
+  if (q->shape[3] == 128 || q->shape[3] == 64) bytes += rows * q->shape[3] * sizeof(float);  // fp32 dQ accumulator
   return bytes;
 }
 
@@ -403,22 +403,42 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     return v && v[0] == '1' ? 1 : 0;
   }();
   g_force_split_bwd = force_split;
-  const bool fused = D == 128 && duq == nullptr && !g_force_split_bwd;
+  const bool fused = !g_force_split_bwd && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
   if (fused) {
     float* acc = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(delta) +
                                           ((size_t)B * H * N * sizeof(float) + 255) / 256 * 256);
     fb_tensor tacc{};
     tacc.data = acc;
-    tacc.shape[0] = B; tacc.shape[1] = H; tacc.shape[2] = N; tacc.shape[3] = 128;
-    tacc.stride[3] = 1; tacc.stride[2] = 128; tacc.stride[1] = (int64_t)N * 128; tacc.stride[0] = (int64_t)H * N * 128;
+    tacc.shape[0] = B; tacc.shape[1] = H; tacc.shape[2] = N; tacc.shape[3] = D;
+    tacc.stride[3] = 1; tacc.stride[2] = D; tacc.stride[1] = (int64_t)N * D; tacc.stride[0] = (int64_t)H * N * D;
     tacc.dtype = FB_F32;
     CUtensorMap macc;
-    if ((rc = make_map(&macc, &tacc, 128, 32, 0, "dq_acc"))) return rc;
-    e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * 128 * sizeof(float), s);
+    if ((rc = make_map(&macc, &tacc, D, 32, 0, "dq_acc"))) return rc;
+    e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * D * sizeof(float), s);
     if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
-    e = launch_bwd_fused_sm100(rp, bias != nullptr, q->dtype == FB_BF16, maps, macc, p, s);
+    if (D == 128) {
+      e = launch_bwd_fused_sm100(rp, bias != nullptr, q->dtype == FB_BF16, maps, macc, p, s);
+    } else {
+      CUtensorMap mduq;
+      memset(&mduq, 0, sizeof(mduq));
+      if (uq) {
+        if ((rc = make_map(&maps.uq64w, uq, 64, 64, 128, "uq"))) return rc;
+        if ((rc = make_map(&maps.uk128w, uk, 64, 128, 128, "uk"))) return rc;
+      }
+      if (duq) {
+        if (duq->stride[3] != 1 || duq->shape[3] != uq->shape[3]) return fail(FB_ESHAPE, "duq layout");
+        if ((rc = make_map(&mduq, duq, (int)duq->shape[3], 32, 0, "duq"))) return rc;
+        for (int64_t bb = 0; bb < duq->shape[0]; ++bb)  // TMA-reduced into: start from zero
+          for (int64_t hh = 0; hh < duq->shape[1]; ++hh) {
+            e = cudaMemsetAsync(static_cast<float*>(duq->data) + bb * duq->stride[0] + hh * duq->stride[1], 0,
+                                (size_t)duq->shape[2] * duq->stride[2] * sizeof(float), s);
+            if (e != cudaSuccess) return cuda_fail(e, "memset duq");
+          }
+      }
+      e = launch_bwd_fused64_sm100(rp, bias != nullptr, q->dtype == FB_BF16, duq != nullptr, maps, macc, mduq, p, s);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "bwd_fused_sm100");
-    e = launch_dq_convert(acc, p, q->dtype == FB_BF16, s);
+    e = launch_dq_convert(acc, D, p, q->dtype == FB_BF16, s);
     note_launch(2);
     return e == cudaSuccess ? FB_OK : cuda_fail(e, "dq_convert");
   }

@@ -52,6 +52,8 @@ struct BwdMaps {
   CUtensorMap q64, do64, uq64, biasT, k128, v128, uk128;
   // dQ kernel: resident 128-row query side, streamed 64-row key-side boxes
   CUtensorMap q128, do128, uq128, bias, k64, v64, uk64;
+  // d=64 fused kernel: factor panels loaded as a second 64-column SW128 atom
+  CUtensorMap uq64w, uk128w;
 };
 
 cudaError_t launch_bwd_sm100(int d, int rp, bool dense, bool bf16, bool factor_grads,
@@ -60,7 +62,11 @@ cudaError_t launch_bwd_sm100(int d, int rp, bool dense, bool bf16, bool factor_g
 // an fp32 accumulator [B,H,N,128] through TMA bulk reductions, then converted
 cudaError_t launch_bwd_fused_sm100(int rp, bool dense, bool bf16, const BwdMaps& maps, const CUtensorMap& dqacc,
                                    const BwdParams& p, cudaStream_t s);
-cudaError_t launch_dq_convert(const float* acc, const BwdParams& p, bool bf16, cudaStream_t s);
+cudaError_t launch_dq_convert(const float* acc, int d, const BwdParams& p, bool bf16, cudaStream_t s);
+// single-pass backward for d = 64 (optionally with factor gradients, Rpad <= 64)
+cudaError_t launch_bwd_fused64_sm100(int rp, bool dense, bool bf16, bool fgrad, const BwdMaps& maps,
+                                     const CUtensorMap& dqacc, const CUtensorMap& duq, const BwdParams& p,
+                                     cudaStream_t s);
 
 // ----- SIMT fp32 path (K5)
 struct SimtParams {
