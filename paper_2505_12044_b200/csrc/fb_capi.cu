@@ -310,7 +310,10 @@ size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k) {
   if (!q) return 0;
   const size_t rows = (size_t)q->shape[0] * q->shape[1] * q->shape[2];
   size_t bytes = (rows * sizeof(float) + 255) / 256 * 256 + 256;  // delta
-  if (q->shape[3] == 128 || q->shape[3] == 64) bytes += rows * q->shape[3] * sizeof(float);  // fp32 dQ accumulator
+  // fp32 dQ accumulator: [B,H,N,D] or, for the 128x128-tile kernel, [B,H,D,N4] (N4 = N rounded up to 4)
+  const size_t n4 = ((size_t)q->shape[2] + 3) / 4 * 4;
+  if (q->shape[3] == 128 || q->shape[3] == 64)
+    bytes += (size_t)q->shape[0] * q->shape[1] * n4 * q->shape[3] * sizeof(float);
   return bytes;
 }
 
@@ -416,7 +419,28 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     if ((rc = make_map(&macc, &tacc, D, 32, 0, "dq_acc"))) return rc;
     e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * D * sizeof(float), s);
     if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
-    if (D == 128) {
+    static const int t128_off = [] {
+      const char* v = getenv("FB_BWD_T128");
+      return v && v[0] == '0' ? 1 : 0;
+    }();
+    if (!t128_off && bwd_t128_supported(D, rp, bias != nullptr, duq != nullptr)) {
+      // transposed accumulator [B,H,D,N4]: 16-query x 128-dim boxes, 64-byte swizzle
+      const int64_t n4 = ((int64_t)N + 3) / 4 * 4;
+      fb_tensor tt{};
+      tt.data = acc;
+      tt.shape[0] = B; tt.shape[1] = H; tt.shape[2] = D; tt.shape[3] = N;
+      tt.stride[3] = 1; tt.stride[2] = n4; tt.stride[1] = n4 * D; tt.stride[0] = n4 * D * H;
+      tt.dtype = FB_F32;
+      CUtensorMap macc_t;
+      if ((rc = make_map(&macc_t, &tt, 16, 128, 64, "dq_acc_t"))) return rc;
+      e = cudaMemsetAsync(acc, 0, (size_t)B * H * n4 * D * sizeof(float), s);
+      if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
+      e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, maps, macc_t, p, s);
+      if (e != cudaSuccess) return cuda_fail(e, "bwd_t128_sm100");
+      e = launch_dq_convert_t(acc, (int)n4, p, q->dtype == FB_BF16, s);
+      note_launch(2);
+      return e == cudaSuccess ? FB_OK : cuda_fail(e, "dq_convert_t");
+    } else if (D == 128) {
       e = launch_bwd_fused_sm100(rp, bias != nullptr, q->dtype == FB_BF16, maps, macc, p, s);
     } else {
       CUtensorMap mduq;

@@ -1,0 +1,57 @@
+// mufu_rate.cu — per-SM throughput of ex2.approx (MUFU), the FMA-pipe
+// polynomial ex2 (ex2_poly2) and packed FFMA2, at 4/8/16 warps per SM.
+#include <cuda.h>
+#include <stdio.h>
+#include "../../paper_2505_12044_b200/csrc/fb_sm100.cuh"
+using namespace fb;
+
+template <int MODE>
+__global__ void k(int iters, float* out, unsigned long long* cyc) {
+  float x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = -0.001f * (threadIdx.x + i);
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) {
+      if (MODE == 0) {
+        x[i] = ex2(x[i]) - 1.0f;
+        x[i + 1] = ex2(x[i + 1]) - 1.0f;
+      } else if (MODE == 1) {
+        float2 r = ex2_poly2(make_float2(x[i], x[i + 1]));
+        x[i] = r.x - 1.0f;
+        x[i + 1] = r.y - 1.0f;
+      } else {
+        float2 r = ffma2(make_float2(x[i], x[i + 1]), make_float2(0.999f, 0.999f), make_float2(1e-7f, 1e-7f));
+        x[i] = r.x;
+        x[i + 1] = r.y;
+      }
+    }
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i];
+  if (s == 12345.f) out[0] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+template <int MODE>
+void run(const char* nm, int warps) {
+  float* o; unsigned long long* c;
+  cudaMalloc(&o, 4); cudaMalloc(&c, 148 * 8);
+  const int iters = 4096;
+  k<MODE><<<148, warps * 32>>>(iters, o, c);
+  cudaDeviceSynchronize();
+  unsigned long long h[148]; cudaMemcpy(h, c, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
+  const double elems = (double)iters * 16 * warps * 32;
+  printf("%-10s warps/SM=%2d: %.2f elements/clk/SM\n", nm, warps, elems / avg);
+}
+
+int main() {
+  for (int w : {4, 8, 16}) { run<0>("ex2 MUFU", w); run<1>("ex2 poly", w); run<2>("FFMA2", w); }
+  return 0;
+}
