@@ -42,6 +42,9 @@
 #ifndef T128_DRAIN_MODE
 #define T128_DRAIN_MODE 0  // experiments only: 1 = plain TMA store instead of reduce-add, 2 = no global write
 #endif
+#ifndef T128_QCHUNK
+#define T128_QCHUNK 16  // queries per dQ reduce-add box (16 KB of stages: 16 -> 2 x 8 KB SW64, 8 -> 4 x 4 KB SW32)
+#endif
 static_assert(2 * T128_REG_EW + T128_REG_DR + T128_REG_OT <= 512, "t128 register pool");
 
 namespace fb {
@@ -64,7 +67,8 @@ __device__ __forceinline__ uint32_t opaque_u32(uint32_t x) {
   asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
   return r;
 }
-__device__ __forceinline__ void t128_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void t128_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void t128_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 }  // namespace
 
@@ -425,16 +429,17 @@ __global__ void __launch_bounds__(512, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->dq_free);
+      constexpr int QC = T128_QCHUNK, RB = QC * 4, NST = 16384 / (128 * RB);  // row bytes, stages
 #pragma unroll
-      for (int c = 0; c < 8; ++c, ++chunk) {
-        uint8_t* stg = reinterpret_cast<uint8_t*>(dq_stage) + (chunk & 1) * 8192;
-        if (leader) t128_wait_read1();  // the reduction that last read this stage has finished reading
+      for (int c = 0; c < 128 / QC; ++c, ++chunk) {
+        uint8_t* stg = reinterpret_cast<uint8_t*>(dq_stage) + (chunk % NST) * (128 * RB);
+        if (leader) t128_wait_read<NST - 1>();  // the reduction that last read this stage has finished reading
         named_bar_sync(3, 128);
         const float sc = p.scale;
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int e = 16 * c + 4 * c4;
-          *reinterpret_cast<float4*>(stg + dd * 64 + ((c4 ^ ((dd >> 1) & 3)) << 4)) =
+        for (int c4 = 0; c4 < QC / 4; ++c4) {
+          const int e = QC * c + 4 * c4;
+          *reinterpret_cast<float4*>(stg + dd * RB + ((c4 ^ ((dd * RB >> 7) & (RB / 16 - 1))) << 4)) =
               make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
                           __uint_as_float(v[e + 3]) * sc);
         }
@@ -442,10 +447,10 @@ __global__ void __launch_bounds__(512, 1)
         named_bar_sync(3, 128);
         if (leader) {
 #if T128_DRAIN_MODE == 0
-          t128_reduce_add(&tm_dqacc, stg, q0 + 16 * c, 0, h, b);
+          t128_reduce_add(&tm_dqacc, stg, q0 + QC * c, 0, h, b);
 #elif T128_DRAIN_MODE == 1
           asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                           reinterpret_cast<uint64_t>(&tm_dqacc)), "r"(smem_u32(stg)), "r"(q0 + 16 * c), "r"(0),
+                           reinterpret_cast<uint64_t>(&tm_dqacc)), "r"(smem_u32(stg)), "r"(q0 + QC * c), "r"(0),
                        "r"(h), "r"(b) : "memory");
 #endif
           t128_bulk_commit();
@@ -511,6 +516,8 @@ cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, 
     dq_convert_t_kernel<false><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn);
   return cudaGetLastError();
 }
+
+int bwd_t128_qchunk() { return T128_QCHUNK; }
 
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads) {
   return d == 128 && rp <= 1 && !dense && !factor_grads;

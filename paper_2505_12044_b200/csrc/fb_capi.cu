@@ -424,7 +424,7 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
       return v && v[0] == '0' ? 1 : 0;
     }();
     if (!t128_off && bwd_t128_supported(D, rp, bias != nullptr, duq != nullptr)) {
-      // transposed accumulator [B,H,D,N4]: 16-query x 128-dim boxes, 64-byte swizzle
+      // transposed accumulator [B,H,D,N4]: qchunk-query x 128-dim boxes, swizzled to the row width
       const int64_t n4 = ((int64_t)N + 3) / 4 * 4;
       fb_tensor tt{};
       tt.data = acc;
@@ -432,7 +432,7 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
       tt.stride[3] = 1; tt.stride[2] = n4; tt.stride[1] = n4 * D; tt.stride[0] = n4 * D * H;
       tt.dtype = FB_F32;
       CUtensorMap macc_t;
-      if ((rc = make_map(&macc_t, &tt, 16, 128, 64, "dq_acc_t"))) return rc;
+      if ((rc = make_map(&macc_t, &tt, bwd_t128_qchunk(), 128, bwd_t128_qchunk() * 4, "dq_acc_t"))) return rc;
       e = cudaMemsetAsync(acc, 0, (size_t)B * H * n4 * D * sizeof(float), s);
       if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
       e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, maps, macc_t, p, s);

@@ -75,6 +75,24 @@ __global__ void __launch_bounds__(192, 1) k(const __grid_constant__ CUtensorMap 
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     red_bytes = n;
+  } else if ((MODE == 6 || MODE == 7) && w >= 2) {
+    unsigned long long n = 0;
+    const int tt = t - 64;  // 0..127: warp wq = tt>>5 handles rows 8*wq.. ; lane -> row (lane>>2), column group (lane&3)
+    const int lane = tt & 31, wq = tt >> 5;
+    while (!done) {
+#pragma unroll 4
+      for (int i = 0; i < 8; ++i) {
+        if (MODE == 6) {
+          float* p = g + static_cast<int64_t>(rbase + 8 * ((wq + 4 * i) & 15) + (lane >> 2)) * 128 + (lane & 3) * 4 + 16 * (i >> 2);
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1.f), "f"(1.f), "f"(1.f), "f"(1.f) : "memory");
+        } else {
+          float* p = g + static_cast<int64_t>(rbase + 8 * ((wq + 4 * i) & 15) + (lane >> 2)) * 128 + (lane & 3) * 2 + 8 * (i >> 2);
+          asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1.f), "f"(1.f) : "memory");
+        }
+      }
+      n += 8 * (MODE == 6 ? 16 : 8);
+    }
+    atomicAdd(&red_bytes, n);
   } else if ((MODE == 2 || MODE == 3) && w >= 2) {
     unsigned long long n = 0;
     const int tt = t - 64;  // 0..127
@@ -119,7 +137,7 @@ void run(const char* name) {
   cfg.gridDim = dim3(148); cfg.blockDim = dim3(192); cfg.dynamicSmemBytes = 6 * 16384;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (MODE >= 4) ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[0].val.clusterDim.x = (MODE == 4 || MODE == 5) ? 2 : 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at; cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, k<MODE>, lmap, rmap, g, 200, d);
   cudaLaunchKernelEx(&cfg, k<MODE>, lmap, rmap, g, 4000, d);
@@ -137,7 +155,7 @@ int main() {
   run<1>("TMA loads + TMA reduce-add");
   run<2>("TMA loads + red.v4 coalesced");
   run<3>("TMA loads + red.v4 lane=row");
-  run<4>("mcast loads (cluster 2) alone");
-  run<5>("mcast loads + TMA reduce-add");
+  run<6>("TMA loads + red.v4 8 rows x 64B");
+  run<7>("TMA loads + red.v2 8 rows x 32B");
   return 0;
 }
