@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(512, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int c2 = 0; c2 < 32; ++c2) {
-          if ((c2 & 3) == 3) {  // one pair in four on the FMA pipe (ex2_poly2), the rest on MUFU
+          if (poly_pair(c2)) {  // FB_POLY_NUM pairs in 8 on the FMA pipe (ex2_poly2), the rest on MUFU
             const float2 e2 = ex2_poly2(make_float2(pr[2 * c2], pr[2 * c2 + 1]));
             pr[2 * c2] = e2.x;
             pr[2 * c2 + 1] = e2.y;

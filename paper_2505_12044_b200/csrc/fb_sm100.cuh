@@ -310,24 +310,36 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 // 2^x for a pair on the FMA/ALU pipes instead of MUFU (FA4-style offload):
 // Cody-Waite split x = r + f (r integer, |f| <= 1/2), 2^f by a degree-3
 // minimax polynomial (max relative error 7.5e-5, below bf16's 3.9e-3), r added
-// straight into the exponent field.  x < -127 (incl. -inf) returns 0.
+// straight into the exponent field.  x is clamped at -125 first (softmax
+// arguments are <= 0; -inf / masked entries give 2^-125 ~ 2.4e-38 instead of 0,
+// far below any bf16/fp32 rounding of the row sums).  11 instructions per pair:
+// 2 FMNMX, 3 FADD2/FFMA2 for the split, 3 FFMA2, 2 IMAD (t's low mantissa bits
+// hold r, and t_bits << 23 == r << 23 mod 2^32 because 0x4B400000 << 23 == 0).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 xc = make_float2(fmaxf(x.x, -125.f), fmaxf(x.y, -125.f));
   const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-  const float2 t = fadd2(xc, magic);                          // r in t's low mantissa bits
+  const float2 t = fadd2(xc, magic);
   const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = ffma2(r, make_float2(-1.f, -1.f), xc);
   float2 p = ffma2(f, make_float2(0.055171619714035273f, 0.055171619714035273f),
                    make_float2(0.2426111703820135f, 0.2426111703820135f));
   p = ffma2(p, f, make_float2(0.6932609990852712f, 0.6932609990852712f));
   p = ffma2(p, f, make_float2(0.9999280709467429f, 0.9999280709467429f));
-  const int ex0 = (__float_as_int(t.x) - 0x4B400000) << 23;
-  const int ex1 = (__float_as_int(t.y) - 0x4B400000) << 23;
   float2 out;
-  out.x = x.x < -127.f ? 0.f : __int_as_float(__float_as_int(p.x) + ex0);
-  out.y = x.y < -127.f ? 0.f : __int_as_float(__float_as_int(p.y) + ex1);
+  out.x = __int_as_float(__float_as_int(p.x) + __float_as_int(t.x) * 0x800000);
+  out.y = __int_as_float(__float_as_int(p.y) + __float_as_int(t.y) * 0x800000);
   return out;
 }
+
+// Which exp2 pairs go through ex2_poly2: FB_POLY_NUM of every 8 (spread out),
+// the rest through MUFU.  MUFU.EX2 is 16/clk/SM (tests/gpu_probe/mufu_rate.cu).
+// Measured on C3 (interleaved A/B runs on one box, power-capped clocks): 0/8
+// 975 TF/s, 1/8 957, 2/8 949-957, 3/8 942, 4/8 930 -- under sw_power_cap the
+// extra FMA-pipe instructions cost more clock than the MUFU time they save.
+#ifndef FB_POLY_NUM
+#define FB_POLY_NUM 0
+#endif
+__host__ __device__ constexpr bool poly_pair(int c) { return ((c & 7) * FB_POLY_NUM) % 8 < FB_POLY_NUM; }
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
