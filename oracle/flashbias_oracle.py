@@ -213,3 +213,31 @@ def svd_decompose(b, rank: Optional[int] = None, energy: Optional[float] = None)
     rep = {"rank_used": k, "energy_retained": float(prof[k - 1]), "max_abs_err": float(np.abs(diff).max()),
            "rel_fro_err": float(np.linalg.norm(diff) / nb) if nb > 0 else 0.0}
     return fq, fk, rep
+
+
+# ---------------------------------------------------------------- head splitting
+def split_heads_by_rank(biases, energy_threshold: float, max_rank: int):
+    """Rank-based head partition (ref: decompose.py:179-225): a head is "low"
+    when the smallest rank retaining ``energy_threshold`` of its energy is
+    <= max_rank; low heads share the subset's maximum rank rounded up to a
+    multiple of 8, with factors U sqrt(s), V sqrt(s) zero-padded to it.
+    Returns (low_indices, [(fq, fk)], dense_indices, common_rank)."""
+    mats = [np.asarray(b, np.float64) for b in biases]
+    svds = [np.linalg.svd(b, full_matrices=False) for b in mats]
+    ranks = [int(np.searchsorted(energy_profile(s), energy_threshold) + 1) for _, s, _ in svds]
+    low = [i for i, r in enumerate(ranks) if r <= max_rank]
+    dense = [i for i in range(len(mats)) if i not in low]
+    if not low:
+        return [], [], dense, 0
+    common = (max(ranks[i] for i in low) + 7) // 8 * 8
+    factors = []
+    for i in low:
+        u, s, vt = svds[i]
+        k_eff = min(common, len(s))
+        root = np.sqrt(s[:k_eff])
+        fq, fk = u[:, :k_eff] * root, vt[:k_eff].T * root
+        if k_eff < common:
+            fq = np.hstack([fq, np.zeros((fq.shape[0], common - k_eff))])
+            fk = np.hstack([fk, np.zeros((fk.shape[0], common - k_eff))])
+        factors.append((fq, fk))
+    return low, factors, dense, common

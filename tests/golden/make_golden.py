@@ -208,6 +208,57 @@ def main() -> None:
     arrays["rng/integers_123"] = R.Rng(123).integers(0, 100, 6).astype(np.float64)
     arrays["rng/normal_big"] = R.Rng(2 ** 40 + 3).normal(3, 2)
 
+    # ---- acceptance criterion 9: head splitting / mixed path (test_acceptance.py:204-236)
+    rng = R.Rng(77)
+    n9 = 64
+    heads = [rng.normal(n9, rank) @ rng.normal(n9, rank).T for rank in (1, 2, 4, 4, 8, 8)]
+    for pos in (2, 5):
+        heads.insert(pos, rng.normal(n9, n9))
+    split = R.split_heads_by_rank(heads, 0.95, max_rank=16)
+    q, k, v = rng.normal(n9, 16), rng.normal(n9, 16), rng.normal(n9, 16)
+    arrays["crit9/heads"] = np.stack(heads)
+    arrays["crit9/q"], arrays["crit9/k"], arrays["crit9/v"] = q, k, v
+    arrays["crit9/low_indices"] = np.asarray(split.low_indices, dtype=np.int64)
+    arrays["crit9/dense_indices"] = np.asarray(split.dense_indices, dtype=np.int64)
+    arrays["crit9/common_rank"] = np.asarray([split.common_rank], dtype=np.int64)
+    factored = dict(zip(split.low_indices, split.low_factors))
+    outs, dense_ref = [], []
+    for idx, head in enumerate(heads):
+        dense_ref.append(R.reference_attention(q, k, v, R.DenseBias(head)))
+        if idx in factored:
+            fb = factored[idx]
+            outs.append(R.flashbias_attention(q, k, v, fb.fq, fb.fk, tiles=R.TileConfig(16, 16)))
+            arrays[f"crit9/fq_{idx}"], arrays[f"crit9/fk_{idx}"] = fb.fq, fb.fk
+        else:
+            outs.append(R.tiled_attention(q, k, v, R.DenseBias(head), tiles=R.TileConfig(16, 16)))
+    arrays["crit9/o_mixed"] = np.stack(outs)
+    arrays["crit9/o_dense"] = np.stack(dense_ref)
+    # a second split instance: energy threshold low enough that every head is factored
+    split2 = R.split_heads_by_rank(heads[:3], 0.5, max_rank=64)
+    arrays["crit9b/low_indices"] = np.asarray(split2.low_indices, dtype=np.int64)
+    arrays["crit9b/common_rank"] = np.asarray([split2.common_rank], dtype=np.int64)
+
+    # ---- file formats (fileio.py; test_fileio.py): raw bytes written by the reference
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        def dump(name, writer, obj, **kw):
+            path = os.path.join(td, name)
+            writer(path, obj, **kw)
+            with open(path, "rb") as f:
+                arrays[f"fileio/{name}"] = np.frombuffer(f.read(), dtype=np.uint8).copy()
+        a = R.Rng(0).normal(7, 5)
+        arrays["fileio/a"] = a
+        dump("a_f64.dbm", R.write_dbm1, a)
+        dump("a_f32.dbm", R.write_dbm1, a, dtype="f32")
+        fb = R.random_low_rank_factors(9, 6, 3, seed=2)
+        arrays["fileio/fq"], arrays["fileio/fk"] = fb.fq, fb.fk
+        dump("f_f64.fbf", R.write_fbf1, fb)
+        dump("f_f32.fbf", R.write_fbf1, fb, dtype="f32")
+        dump("neural.fbf", R.write_fbf1, R.FactoredBias(np.ones((2, 1)), np.ones((3, 1)), origin="neural"))
+        fs = R.decompose_alibi(32, 32, slope=-0.25)
+        arrays["fileio/alibi_fq"], arrays["fileio/alibi_fk"] = fs.fq, fs.fk
+        dump("alibi_exact.fbf", R.write_fbf1, fs)
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump({"source": "reference flashbias 0.1.0 (pkg/src/flashbias), generated by make_golden.py",
