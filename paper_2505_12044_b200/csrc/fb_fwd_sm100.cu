@@ -53,10 +53,14 @@ struct FwdCfg {
   static_assert(kSlots >= 2, "shared memory ring too small");
 };
 
+// P split: the first kSplitPairs packed columns (96 keys) feed PV K-steps 0..kSplitSteps-1
+constexpr int kSplitPairs = 48, kSplitSteps = 6;
+
 struct FwdBars {
   uint64_t q_full;
   uint64_t s_full[2];
   uint64_t p_ready[2];
+  uint64_t p_part[2];  // first kSplitPairs bf16 pairs of P written (PV K-steps 0..5 may start)
   uint64_t o_final[2];
   uint64_t slot_full[8];
   uint64_t slot_empty[8];
@@ -119,6 +123,7 @@ __global__ void __launch_bounds__(384, 1)
     for (int t = 0; t < 2; ++t) {
       mbar_init(&bars->s_full[t], 1);
       mbar_init(&bars->p_ready[t], 4);
+      mbar_init(&bars->p_part[t], 4);
       mbar_init(&bars->o_final[t], 1);
     }
     for (int s = 0; s < Cfg::kSlots; ++s) {
@@ -220,15 +225,24 @@ __global__ void __launch_bounds__(384, 1)
                  make_sdesc(kb + Cfg::kQBytes + pn * Cfg::kPanelBytes, 16, 256, 6), idesc_qk, 1u);
         tc_commit(&bars->s_full[t]);
       };
-      auto issue_pv = [&](int t, int vitem, bool acc) {
-        trace(p.trace, p.trace_cta, 3, t * 1024 + vitem);
+      // PV in two parts (FA4-style split arrive): K-steps over the first 96 keys
+      // start once the softmax has written that part of P, the last 32 after p_ready
+      auto issue_pv = [&](int t, int vitem, bool acc, uint32_t parity) {
         const uint32_t d_o = tmem + 256 + t * D;
         const uint32_t a_p = tmem + t * 128;
         const uint32_t vb = slot_addr(vitem);
+        mbar_wait(&bars->p_part[t], parity);
+        tc_fence_after();
+        trace(p.trace, p.trace_cta, 3, t * 1024 + vitem);
 #pragma unroll
-        for (int kk = 0; kk < kTileRows / 16; ++kk)
+        for (int kk = 0; kk < kSplitSteps; ++kk)
           mma_ts(d_o, a_p + kk * 8, mnmajor_desc(vb, kTileRows, Cfg::kSW, kk * 16), idesc_pv,
                  (acc || kk > 0) ? 1u : 0u);
+        mbar_wait(&bars->p_ready[t], parity);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = kSplitSteps; kk < kTileRows / 16; ++kk)
+          mma_ts(d_o, a_p + kk * 8, mnmajor_desc(vb, kTileRows, Cfg::kSW, kk * 16), idesc_pv, 1u);
       };
       auto v_item = [&](int st) { return step_base(st) + step_items(st) - 1; };
 
@@ -247,9 +261,7 @@ __global__ void __launch_bounds__(384, 1)
         const int vi = v_item(st);
         wait_full(vi);
         if (st >= dlt) {
-          mbar_wait(&bars->p_ready[0], (st - dlt) & 1);
-          tc_fence_after();
-          issue_pv(0, vi, st > dlt);
+          issue_pv(0, vi, st > dlt, (st - dlt) & 1);
           if (st + 1 < n1) {
             wait_full(step_base(st + 1));
             issue_s(0, st + 1);
@@ -257,9 +269,7 @@ __global__ void __launch_bounds__(384, 1)
             tc_commit(&bars->o_final[0]);
           }
         }
-        mbar_wait(&bars->p_ready[1], st & 1);
-        tc_fence_after();
-        issue_pv(1, vi, st > 0);
+        issue_pv(1, vi, st > 0, st & 1);
         release(vi);
         if (st + 1 < n1) {
           wait_full(step_base(st + 1));
@@ -357,27 +367,8 @@ __global__ void __launch_bounds__(384, 1)
         alpha = ex2(m_run - m_new);
         m_run = m_new;
       }
-      // p = 2^(x*sl2 - m): packed FFMA2, MUFU ex2, packed FADD2 partial sums
-      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      {
-        const float2 mul = DENSE ? make_float2(1.f, 1.f) : make_float2(sl2, sl2);
-        const float2 neg = make_float2(-m_run, -m_run);
-        uint32_t pk[64];
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float2 e2 = ffma2(make_float2(x[2 * c], x[2 * c + 1]), mul, neg);
-          // FB_POLY_NUM pairs in 8 go through the FMA-pipe polynomial, the rest through MUFU
-          const float2 p2 = poly_pair(c) ? ex2_poly2(e2) : make_float2(ex2(e2.x), ex2(e2.y));
-          acc[c & 3] = fadd2(acc[c & 3], p2);
-          pk[c] = pack2<BF16>(p2.x, p2.y);
-        }
-        tmem_st32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(pk + 0));
-        tmem_st32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(pk + 32));
-      }
-      const float2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
-      const float2 s4 = fadd2(s01, s23);
-      l_run = l_run * alpha + (s4.x + s4.y);
-      // O_t was last written by PV_t(previous), which completed before S_t(this) (commit order)
+      // O_t was last written by PV_t(previous), which completed before S_t(this)
+      // (commit order): rescale it now, before any part of P is released to PV_t(this)
       if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
         for (int c0 = 0; c0 < D; c0 += 32) {
@@ -393,7 +384,35 @@ __global__ void __launch_bounds__(384, 1)
           }
           tmem_st32(t_o + c0, o);
         }
+        tmem_wait_st();
       }
+      // p = 2^(x*sl2 - m): packed FFMA2, MUFU ex2, packed FADD2 partial sums
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      {
+        const float2 mul = DENSE ? make_float2(1.f, 1.f) : make_float2(sl2, sl2);
+        const float2 neg = make_float2(-m_run, -m_run);
+        uint32_t pk[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float2 e2 = ffma2(make_float2(x[2 * c], x[2 * c + 1]), mul, neg);
+          // FB_POLY_NUM pairs in 8 go through the FMA-pipe polynomial, the rest through MUFU
+          const float2 p2 = poly_pair(c) ? ex2_poly2(e2) : make_float2(ex2(e2.x), ex2(e2.y));
+          acc[c & 3] = fadd2(acc[c & 3], p2);
+          pk[c] = pack2<BF16>(p2.x, p2.y);
+          if (c == kSplitPairs - 1) {  // first 3/4 of P -> TMEM, release PV K-steps 0..5
+            tmem_st32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(pk + 0));
+            tmem_st16(t_s + 32, *reinterpret_cast<uint32_t(*)[16]>(pk + 32));
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->p_part[t]);
+          }
+        }
+        tmem_st16(t_s + 48, *reinterpret_cast<uint32_t(*)[16]>(pk + 48));
+      }
+      const float2 s01 = fadd2(acc[0], acc[1]), s23 = fadd2(acc[2], acc[3]);
+      const float2 s4 = fadd2(s01, s23);
+      l_run = l_run * alpha + (s4.x + s4.y);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
