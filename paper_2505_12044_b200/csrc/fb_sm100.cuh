@@ -340,6 +340,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 #define FB_POLY_NUM 0
 #endif
 __host__ __device__ constexpr bool poly_pair(int c) { return ((c & 7) * FB_POLY_NUM) % 8 < FB_POLY_NUM; }
+// forward softmax (MUFU-heavy: 16384 ex2 per 128x128 tile against ~1088 tensor cycles)
+#ifndef FB_POLY_NUM_FWD
+#define FB_POLY_NUM_FWD 0
+#endif
+__host__ __device__ constexpr bool poly_pair_fwd(int c) { return ((c & 7) * FB_POLY_NUM_FWD) % 8 < FB_POLY_NUM_FWD; }
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;

@@ -2,6 +2,8 @@
 // polynomial ex2 (ex2_poly2) and packed FFMA2, at 4/8/16 warps per SM.
 #include <cuda.h>
 #include <stdio.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
 #include "../../paper_2505_12044_b200/csrc/fb_sm100.cuh"
 using namespace fb;
 
@@ -22,6 +24,22 @@ __global__ void k(int iters, float* out, unsigned long long* cyc) {
         float2 r = ex2_poly2(make_float2(x[i], x[i + 1]));
         x[i] = r.x - 1.0f;
         x[i + 1] = r.y - 1.0f;
+      } else if (MODE == 3) {  // ex2.approx.f16x2: one MUFU op per lane for two fp16 values?
+        __half2 h = __floats2half2_rn(x[i], x[i + 1]);
+        uint32_t u = *reinterpret_cast<uint32_t*>(&h), o;
+        asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(o) : "r"(u));
+        __half2 ho = *reinterpret_cast<__half2*>(&o);
+        float2 f = __half22float2(ho);
+        x[i] = f.x - 1.0f;
+        x[i + 1] = f.y - 1.0f;
+      } else if (MODE == 4) {  // ex2.approx.ftz.bf16x2
+        __nv_bfloat162 h = __floats2bfloat162_rn(x[i], x[i + 1]);
+        uint32_t u = *reinterpret_cast<uint32_t*>(&h), o;
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(o) : "r"(u));
+        __nv_bfloat162 ho = *reinterpret_cast<__nv_bfloat162*>(&o);
+        float2 f = __bfloat1622float2(ho);
+        x[i] = f.x - 1.0f;
+        x[i + 1] = f.y - 1.0f;
       } else {
         float2 r = ffma2(make_float2(x[i], x[i + 1]), make_float2(0.999f, 0.999f), make_float2(1e-7f, 1e-7f));
         x[i] = r.x;
@@ -52,6 +70,6 @@ void run(const char* nm, int warps) {
 }
 
 int main() {
-  for (int w : {4, 8, 16}) { run<0>("ex2 MUFU", w); run<1>("ex2 poly", w); run<2>("FFMA2", w); }
+  for (int w : {4, 8, 16}) { run<0>("ex2 MUFU", w); run<1>("ex2 poly", w); run<2>("FFMA2", w); run<3>("ex2 f16x2", w); run<4>("ex2 bf16x2", w); }
   return 0;
 }
