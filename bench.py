@@ -243,7 +243,7 @@ def kernel_breakdown(cfg, inp, reps: int = 3):
     d = cfg["d"]
     q, k, v, do = (t.detach() for t in (inp["q"], inp["k"], inp["v"], inp["do"]))
     premul = math.sqrt(d)
-    split = A.choose_split(inp["fq"], inp["fk"], premul)
+    split = A.choose_split_cached(inp["fq"], inp["fk"], premul, max_cols=64 if d == 128 else 128)  # as the step
     uq, uk = A.prepare_factor_panels(inp["fq"].detach(), inp["fk"].detach(), premul, split, q.dtype)
     scale = 1.0 / math.sqrt(d)
     out = {}

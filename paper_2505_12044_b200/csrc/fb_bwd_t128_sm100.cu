@@ -484,32 +484,42 @@ static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, con
   return cudaGetLastError();
 }
 
-// dq[b,h,n,:] = acc_t[b,h,:,n]: 32-query x 128-dim tiles transposed through shared memory
+// dq[b,h,n,:] = acc_t[b,h,:,n]: 64-query x 128-dim tiles transposed through
+// shared memory; float4 loads along queries, 16-byte bf16 stores along the head dim.
 template <bool BF16>
-__global__ void __launch_bounds__(256) dq_convert_t_kernel(const float* __restrict__ acc, void* dq, int H, int N, int n4,
-                                                           int64_t sb, int64_t sh, int64_t sn) {
+__global__ void __launch_bounds__(256) dq_convert_t_kernel(const float* __restrict__ acc, void* dq, int H, int N,
+                                                           int n4, int64_t sb, int64_t sh, int64_t sn) {
   typedef typename std::conditional<BF16, __nv_bfloat16, __half>::type elem_t;
-  __shared__ float tile[128][33];
-  const int bh = blockIdx.y, q0 = blockIdx.x * 32;
+  __shared__ float tile[64][129];  // [query][dim], odd stride
+  const int bh = blockIdx.y, q0 = blockIdx.x * 64;
   const int bb = bh / H, hh = bh % H;
   const float* src = acc + static_cast<int64_t>(bh) * 128 * n4;
   const int t = threadIdx.x;
-  for (int i = t; i < 128 * 32; i += 256) {  // coalesced along queries
-    const int d = i >> 5, qq = i & 31;
-    tile[d][qq] = q0 + qq < N ? src[static_cast<int64_t>(d) * n4 + q0 + qq] : 0.f;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {  // 128 dims x 16 float4 (64 queries)
+    const int i = it * 256 + t, d = i >> 4, q4 = (i & 15) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q0 + q4 + 3 < n4) v = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(d) * n4 + q0 + q4);
+    tile[q4][d] = v.x;
+    tile[q4 + 1][d] = v.y;
+    tile[q4 + 2][d] = v.z;
+    tile[q4 + 3][d] = v.w;
   }
   __syncthreads();
   elem_t* dst = reinterpret_cast<elem_t*>(dq) + static_cast<int64_t>(bb) * sb + static_cast<int64_t>(hh) * sh;
-  for (int i = t; i < 32 * 64; i += 256) {  // coalesced along the head dim, 2 elements per thread
-    const int qq = i >> 6, d2 = (i & 63) * 2;
-    if (q0 + qq < N)
-      *reinterpret_cast<uint32_t*>(dst + static_cast<int64_t>(q0 + qq) * sn + d2) =
-          pack2<BF16>(tile[d2][qq], tile[d2 + 1][qq]);
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {  // 64 queries x 16 chunks of 8 dims
+    const int i = it * 256 + t, qq = i >> 4, d8 = (i & 15) * 8;
+    if (q0 + qq < N) {
+      const float* r = &tile[qq][d8];
+      *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(q0 + qq) * sn + d8) =
+          make_uint4(pack2<BF16>(r[0], r[1]), pack2<BF16>(r[2], r[3]), pack2<BF16>(r[4], r[5]), pack2<BF16>(r[6], r[7]));
+    }
   }
 }
 
 cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, bool bf16, cudaStream_t s) {
-  dim3 grid((p.N + 31) / 32, p.B * p.H);
+  dim3 grid((p.N + 63) / 64, p.B * p.H);
   if (bf16)
     dq_convert_t_kernel<true><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn);
   else

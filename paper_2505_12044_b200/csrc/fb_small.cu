@@ -59,35 +59,90 @@ __device__ __forceinline__ float split_part(float x, int part, int dtype) {
 }
 
 // ------------------------------------------------------------ K6 split
+// grid (ceil(L*rpad / 256), B*H): 32-bit index math inside one [L, rpad] plane
+// (the 64-bit div/mod chain per element made this launch-latency-scale kernel
+// cost 15-25 us at C2/C4 sizes).
 __global__ void prepare_factors_kernel(Tensor4 f, int side, int split, float premul, Tensor4 out) {
   const int R = static_cast<int>(f.shape[3]);
   const int np = (split * (split + 1)) / 2;
-  const int64_t L = out.shape[2], Hh = out.shape[1], Bb = out.shape[0];
-  const int64_t rpad = out.shape[3];
-  const int64_t total = Bb * Hh * L * rpad;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t c = idx % rpad;
-    const int64_t l = (idx / rpad) % L;
-    const int64_t h = (idx / (rpad * L)) % Hh;
-    const int64_t b = idx / (rpad * L * Hh);
+  const int L = static_cast<int>(out.shape[2]), Hh = static_cast<int>(out.shape[1]);
+  const int rpad = static_cast<int>(out.shape[3]);
+  const int plane = blockIdx.y;
+  const int64_t b = plane / Hh, h = plane % Hh;
+  const float mul = side == 0 ? premul : 1.0f;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < L * rpad; idx += gridDim.x * blockDim.x) {
+    const int c = idx % rpad, l = idx / rpad;
     float v = 0.f;
-    if (c < static_cast<int64_t>(R) * np) {
-      const int r = static_cast<int>(c / np);
+    if (c < R * np) {
+      const int r = c / np;
       int a, bpart;
-      pair_parts(static_cast<int>(c % np), a, bpart);
-      const float x = load_elem(f.data, off4(f, b, h, l, r), f.dtype) * (side == 0 ? premul : 1.0f);
+      pair_parts(c % np, a, bpart);
+      const float x = load_elem(f.data, off4(f, b, h, l, r), f.dtype) * mul;
       v = split_part(x, side == 0 ? a : bpart, out.dtype);
     }
     store_elem(out.data, off4(out, b, h, l, c), out.dtype, v);
   }
 }
 
+// Fast path: one thread per 8-column chunk of a panel row, one 16-byte store.
+template <bool BF16>
+__global__ void __launch_bounds__(256) prepare_factors_rows_kernel(Tensor4 f, int side, int split, float premul,
+                                                                   Tensor4 out) {
+  const int R = static_cast<int>(f.shape[3]);
+  const int np = (split * (split + 1)) / 2;
+  const int L = static_cast<int>(out.shape[2]), Hh = static_cast<int>(out.shape[1]);
+  const int nch = static_cast<int>(out.shape[3]) / 8;
+  const int plane = blockIdx.y;
+  const int64_t b = plane / Hh, h = plane % Hh;
+  const float mul = side == 0 ? premul : 1.0f;
+  const int odt = BF16 ? 1 : 2;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < L * nch; idx += gridDim.x * blockDim.x) {
+    const int l = idx / nch, c8 = (idx % nch) * 8;
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float v2[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int c = c8 + 2 * e + k;
+        float v = 0.f;
+        if (c < R * np) {
+          int a, bp;
+          pair_parts(c % np, a, bp);
+          v = split_part(load_elem(f.data, off4(f, b, h, l, c / np), f.dtype) * mul, side == 0 ? a : bp, odt);
+        }
+        v2[k] = v;
+      }
+      w[e] = pack2<BF16>(v2[0], v2[1]);
+    }
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(out.data) + off4(out, b, h, l, c8)) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
 cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul,
                                    const Tensor4& out, cudaStream_t s) {
-  const int64_t total = out.shape[0] * out.shape[1] * out.shape[2] * out.shape[3];
-  const int grid = static_cast<int>((total + 255) / 256 > 148 * 16 ? 148 * 16 : (total + 255) / 256);
-  prepare_factors_kernel<<<grid > 0 ? grid : 1, 256, 0, s>>>(f, side, split, premul, out);
+  const int64_t per_plane = out.shape[2] * out.shape[3];
+  const int64_t planes = out.shape[0] * out.shape[1];
+  if (per_plane <= 0 || planes <= 0) return cudaSuccess;
+  if (planes > 65535 || per_plane > (int64_t(1) << 30)) return cudaErrorInvalidValue;
+  const bool rows_ok = (out.dtype == 1 || out.dtype == 2) && out.stride[3] == 1 && out.shape[3] % 8 == 0 &&
+                       out.stride[2] % 8 == 0 && out.stride[1] % 8 == 0 && out.stride[0] % 8 == 0 &&
+                       (reinterpret_cast<uintptr_t>(out.data) % 16) == 0;
+  if (rows_ok) {
+    int64_t gx = (out.shape[2] * (out.shape[3] / 8) + 255) / 256;
+    const int64_t cap = (148 * 16 + planes - 1) / planes;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(planes));
+    if (out.dtype == 1) prepare_factors_rows_kernel<true><<<grid, 256, 0, s>>>(f, side, split, premul, out);
+    else prepare_factors_rows_kernel<false><<<grid, 256, 0, s>>>(f, side, split, premul, out);
+  } else {
+    int64_t gx = (per_plane + 255) / 256;
+    const int64_t cap = (148 * 16 + planes - 1) / planes;
+    if (gx > cap) gx = cap < 1 ? 1 : cap;
+    prepare_factors_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(planes)), 256, 0, s>>>(
+        f, side, split, premul, out);
+  }
   note_launch();
   return cudaGetLastError();
 }
@@ -250,12 +305,79 @@ __global__ void bwd_preprocess_kernel(Tensor4 o, Tensor4 dout, Tensor4 delta) {
   }
 }
 
+// Vectorised fast path (bf16/f16, contiguous rows, 16-byte aligned): D/8 threads
+// per row, one 16-byte load of O and dO each, shuffle reduction inside the row
+// group; grid.y = the (b, h) plane.  HBM-bound: reads O and dO once.
+template <typename T, int TPR>
+__global__ void __launch_bounds__(256) bwd_preprocess_vec_kernel(const T* __restrict__ o, const T* __restrict__ dout,
+                                                                 float* __restrict__ delta, int H, int N,
+                                                                 int64_t o_sb, int64_t o_sh, int64_t o_sn,
+                                                                 int64_t d_sb, int64_t d_sh, int64_t d_sn) {
+  constexpr int RPB = 256 / TPR;
+  const int plane = blockIdx.y, b = plane / H, h = plane % H;
+  const int sub = threadIdx.x % TPR;
+  const T* ob = o + b * o_sb + h * o_sh + sub * 8;
+  const T* db = dout + b * d_sb + h * d_sh + sub * 8;
+  for (int i = blockIdx.x * RPB + threadIdx.x / TPR; i < N; i += gridDim.x * RPB) {
+    const uint4 a = *reinterpret_cast<const uint4*>(ob + static_cast<int64_t>(i) * o_sn);
+    const uint4 c = *reinterpret_cast<const uint4*>(db + static_cast<int64_t>(i) * d_sn);
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, cw[4] = {c.x, c.y, c.z, c.w};
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 x = unpack2<std::is_same<T, __nv_bfloat16>::value>(aw[e]);
+      const float2 y = unpack2<std::is_same<T, __nv_bfloat16>::value>(cw[e]);
+      acc = ffma2(x, y, acc);
+    }
+    float sum = acc.x + acc.y;
+#pragma unroll
+    for (int m = TPR / 2; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+    if (sub == 0) delta[static_cast<int64_t>(plane) * N + i] = sum;
+  }
+}
+
+template <typename T>
+static void launch_pre_vec(const Tensor4& o, const Tensor4& dout, const Tensor4& delta, cudaStream_t s) {
+  const int B = static_cast<int>(o.shape[0]), H = static_cast<int>(o.shape[1]), N = static_cast<int>(o.shape[2]);
+  const int D = static_cast<int>(o.shape[3]);
+  const int tpr = D / 8;
+  const int rpb = 256 / tpr;
+  int64_t gx = (N + rpb - 1) / rpb;
+  const int64_t cap = (148 * 8 + B * H - 1) / (B * H);
+  if (gx > cap) gx = cap < 1 ? 1 : cap;
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(B * H));
+  const T* op = reinterpret_cast<const T*>(o.data);
+  const T* dp = reinterpret_cast<const T*>(dout.data);
+  float* dl = reinterpret_cast<float*>(delta.data);
+#define FB_PRE(TPRV)                                                                                        \
+  bwd_preprocess_vec_kernel<T, TPRV><<<grid, 256, 0, s>>>(op, dp, dl, H, N, o.stride[0], o.stride[1], o.stride[2], \
+                                                          dout.stride[0], dout.stride[1], dout.stride[2])
+  if (tpr == 16) FB_PRE(16);
+  else if (tpr == 8) FB_PRE(8);
+  else FB_PRE(4);
+#undef FB_PRE
+}
+
 cudaError_t launch_bwd_preprocess(const Tensor4& o, const Tensor4& dout, const Tensor4& delta,
                                   cudaStream_t s) {
   const int64_t rows = o.shape[0] * o.shape[1] * o.shape[2];
-  int64_t g = (rows + 7) / 8;
-  if (g > 148 * 16) g = 148 * 16;
-  bwd_preprocess_kernel<<<static_cast<int>(g), 256, 0, s>>>(o, dout, delta);
+  if (rows <= 0) return cudaSuccess;
+  const int64_t D = o.shape[3];
+  auto vec_ok = [&](const Tensor4& t) {
+    return t.stride[3] == 1 && (reinterpret_cast<uintptr_t>(t.data) % 16) == 0 && t.stride[2] % 8 == 0 &&
+           t.stride[1] % 8 == 0 && t.stride[0] % 8 == 0;
+  };
+  const bool contig_delta = delta.stride[2] == 1 && delta.stride[1] == o.shape[2] &&
+                            delta.stride[0] == o.shape[1] * o.shape[2];
+  if ((D == 32 || D == 64 || D == 128) && o.dtype == dout.dtype && (o.dtype == 1 || o.dtype == 2) && vec_ok(o) &&
+      vec_ok(dout) && contig_delta && o.shape[0] * o.shape[1] <= 65535 && o.shape[2] < (int64_t(1) << 31)) {
+    if (o.dtype == 1) launch_pre_vec<__nv_bfloat16>(o, dout, delta, s);
+    else launch_pre_vec<__half>(o, dout, delta, s);
+  } else {
+    int64_t g = (rows + 7) / 8;
+    if (g > 148 * 16) g = 148 * 16;
+    bwd_preprocess_kernel<<<static_cast<int>(g), 256, 0, s>>>(o, dout, delta);
+  }
   note_launch();
   return cudaGetLastError();
 }

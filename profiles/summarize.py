@@ -27,6 +27,10 @@ METRICS = [
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("l1tex__m_l1tex2xbar_write_bytes.sum", "SM->L2 write bytes (dQ reduce-adds)"),
+    ("l1tex__m_l1tex2xbar_write_bytes.sum.pct_of_peak_sustained_elapsed", "SM->L2 write % of peak"),
+    ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2->SM read bytes (TMA loads)"),
+    ("lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum", "L2 read hits (sectors)"),
     ("launch__registers_per_thread", "registers/thread"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("launch__grid_size", "grid"),
@@ -85,7 +89,7 @@ def main(tag):
                 k = r[ki].split("(")[0].replace("void ", "")
                 tot[k] = tot.get(k, 0.0) + to_num(r[vi], r[ui])
         s = sum(tot.values())
-        lines += ["## launch list (all fb_ kernels of one bench invocation)", "", "| kernel | total time | share |",
+        lines += ["## launch list (every kernel of one C3 bench step: bench.py --steps 1 --warmup 1, cold-cache serialised replays)", "", "| kernel | total time | share |",
                   "|---|---|---|"]
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
             lines.append(f"| `{k}` | {v * 1e3:.2f} ms | {v / s:.1%} |")
