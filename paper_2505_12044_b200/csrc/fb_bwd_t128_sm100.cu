@@ -40,7 +40,9 @@
 #define T128_REG_OT 72
 #endif
 #ifndef T128_DRAIN_MODE
-#define T128_DRAIN_MODE 0  // experiments only: 1 = plain TMA store instead of reduce-add, 2 = no global write
+#define T128_DRAIN_MODE 0  // 0 = TMA reduce-add from a swizzled smem stage, 3 = red.global.add.v4.f32 after a
+                           // per-warp smem transpose (measured C3 bwd 25.1-25.4 ms vs 23.1 for mode 0);
+                           // experiments: 1 = TMA store (wrong), 2 = no global write
 #endif
 #ifndef T128_QCHUNK
 #define T128_QCHUNK 16  // queries per dQ reduce-add box (16 KB of stages: 16 -> 2 x 8 KB SW64, 8 -> 4 x 4 KB SW32)
@@ -415,6 +417,56 @@ __global__ void __launch_bounds__(512, 1)
     const int dd = threadIdx.x - 256;  // head-dim index = TMEM lane of dQ^T
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const bool leader = dd == 0;
+#if T128_DRAIN_MODE == 3
+    // Per-warp transpose through a private 4 KB scratch (rows = this warp's 32
+    // head dims, 16-byte chunks XOR-swizzled by row), then coalesced
+    // red.global.add.v4.f32: each instruction adds 4 rows x 32 queries (512 B).
+    // No TMA stage to wait on: the scratch is reused as soon as the warp has
+    // read it back, so reductions stay in flight in the memory system.
+    float* acc_bh = p.dq_acc + static_cast<int64_t>(b * p.H + h) * 128 * p.acc_n4;
+    uint8_t* scratch = reinterpret_cast<uint8_t*>(dq_stage) + (warp & 3) * 4096;
+    const int wrow0 = (warp & 3) * 32;
+    for (int j = 0; j < nblk; ++j) {
+      const int q0 = (i_start + j) * 128;
+      mbar_wait(&bars->dq_full, j & 1);
+      tc_fence_after();
+      if (leader) trace(p.trace, p.trace_cta, 19, j);
+      uint32_t v[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tmem_ld32(tmem + lane_off + T_DP + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->dq_free);
+      const float sc = p.scale;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // 32-query rounds
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          const int e = 32 * c + 4 * ch;
+          *reinterpret_cast<float4*>(scratch + lane * 128 + ((ch ^ (lane & 7)) << 4)) =
+              make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
+                          __uint_as_float(v[e + 3]) * sc);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int row = 4 * i + (lane >> 3), ch = lane & 7;
+          const float4 x = *reinterpret_cast<const float4*>(scratch + row * 128 + ((ch ^ (row & 7)) << 4));
+          const int q = q0 + 32 * c + 4 * ch;
+          if (q < p.N) {
+            float* dst = acc_bh + static_cast<int64_t>(wrow0 + row) * p.acc_n4 + q;
+            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(x.x), "f"(x.y), "f"(x.z),
+                         "f"(x.w)
+                         : "memory");
+          }
+        }
+        __syncwarp();
+      }
+      if (leader) trace(p.trace, p.trace_cta, 20, j);
+    }
+#else
     int chunk = 0;
     for (int j = 0; j < nblk; ++j) {
       const int q0 = (i_start + j) * 128;
@@ -458,6 +510,7 @@ __global__ void __launch_bounds__(512, 1)
       }
       if (leader) trace(p.trace, p.trace_cta, 20, j);
     }
+#endif
     if (leader) t128_wait_all();
   }
 

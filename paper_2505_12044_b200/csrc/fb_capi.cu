@@ -435,6 +435,8 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
       if ((rc = make_map(&macc_t, &tt, bwd_t128_qchunk(), 128, bwd_t128_qchunk() * 4, "dq_acc_t"))) return rc;
       e = cudaMemsetAsync(acc, 0, (size_t)B * H * n4 * D * sizeof(float), s);
       if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
+      p.dq_acc = acc;
+      p.acc_n4 = (int)n4;
       e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, maps, macc_t, p, s);
       if (e != cudaSuccess) return cuda_fail(e, "bwd_t128_sm100");
       e = launch_dq_convert_t(acc, (int)n4, p, q->dtype == FB_BF16, s);

@@ -44,6 +44,7 @@ struct BwdParams {
   float* duq; int64_t duq_sb, duq_sh, duq_sn;  // nullable, fp32 [B,H,N,Rpad]
   float* duk; int64_t duk_sb, duk_sh, duk_sn;
   int uq_bb, uq_hb, uk_bb, uk_hb, bias_bb, bias_hb;
+  float* dq_acc; int acc_n4;  // 128x128-tile kernel: transposed fp32 dQ accumulator [B,H,128,acc_n4]
   unsigned long long* trace; int trace_cta;  // FB_TRACE builds only
 };
 
