@@ -241,3 +241,38 @@ def split_heads_by_rank(biases, energy_threshold: float, max_rank: int):
             fk = np.hstack([fk, np.zeros((fk.shape[0], common - k_eff))])
         factors.append((fq, fk))
     return low, factors, dense, common
+
+
+# ---------------------------------------------------------------- neural factor networks
+def mlp_forward(params, x):
+    """Three linear layers, tanh after the first two (ref: neural.py:44-47).
+    params = [w1, w2, w3, b1, b2, b3]."""
+    w1, w2, w3, b1, b2, b3 = params
+    h1 = np.tanh(x @ w1 + b1)
+    h2 = np.tanh(h1 @ w2 + b2)
+    return h2 @ w3 + b3, (x, h1, h2)
+
+
+def factor_loss_and_grads(q_params, k_params, xq, xk, target):
+    """MSE of yq yk^T against target and its gradients (ref: neural.py:49-60, 88-98)."""
+    def back(params, cache, dy):
+        w1, w2, w3 = params[:3]
+        x, h1, h2 = cache
+        dh2 = (dy @ w3.T) * (1.0 - h2 * h2)
+        dh1 = (dh2 @ w2.T) * (1.0 - h1 * h1)
+        return [x.T @ dh1, h1.T @ dh2, h2.T @ dy, dh1.sum(0), dh2.sum(0), dy.sum(0)]
+    yq, cq = mlp_forward(q_params, xq)
+    yk, ck = mlp_forward(k_params, xk)
+    diff = yq @ yk.T - target
+    g = (2.0 / diff.size) * diff
+    return float(np.mean(diff * diff)), back(q_params, cq, g @ yk) + back(k_params, ck, g.T @ yq)
+
+
+def glorot_params(rng, dims):
+    """Reference initialisation (ref: neural.py:31-40) from an Rng-like stream."""
+    ws, bs = [], []
+    for fan_in, fan_out in zip(dims[:-1], dims[1:]):
+        limit = np.sqrt(6.0 / (fan_in + fan_out))
+        ws.append((rng.uniform(fan_in, fan_out) * 2.0 - 1.0) * limit)
+        bs.append(np.zeros(fan_out))
+    return ws + bs

@@ -259,6 +259,41 @@ def main() -> None:
         arrays["fileio/alibi_fq"], arrays["fileio/alibi_fk"] = fs.fq, fs.fk
         dump("alibi_exact.fbf", R.write_fbf1, fs)
 
+    # ---- neural decomposer (neural.py; test_neural.py, test_integration.py:45-54, criterion 4)
+    rng = R.Rng(21)
+    xq, xk = rng.uniform(4, 2), rng.uniform(4, 2)
+    target = rng.normal(4, 4)
+    nets = R.FactorNetworks.init(R.Rng(22), 2, 5, 3)
+    loss, grads = nets.loss_and_grads(xq, xk, target)
+    arrays["neural_grad/xq"], arrays["neural_grad/xk"], arrays["neural_grad/target"] = xq, xk, target
+    arrays["neural_grad/loss"] = np.array([loss])
+    for i, g in enumerate(grads):
+        arrays[f"neural_grad/g{i}"] = g
+    rng = R.Rng(5)
+    xq = rng.uniform(10, 2)
+    target = rng.normal(10, 10)
+    fb, _, losses = R.neural_decompose(xq, xq, target, rank=4, hidden=16, iters=200, lr=1e-3,
+                                       lr_decay=(0.5, 50), seed=1)
+    arrays["neural_fit/xq"], arrays["neural_fit/target"] = xq, target
+    arrays["neural_fit/losses"], arrays["neural_fit/fq"], arrays["neural_fit/fk"] = np.asarray(losses), fb.fq, fb.fk
+    rng = R.Rng(56)
+    ll = np.stack([rng.uniform(48) * np.pi - np.pi / 2, rng.uniform(48) * 2 * np.pi - np.pi], axis=1)
+    target = R.generate_bias(R.SphericalDistanceBias(ll))
+    fb, _, losses = R.neural_decompose(ll, ll, target, rank=8, hidden=32, iters=400, seed=3)
+    rep = R.reconstruction_report(fb, target)
+    arrays["neural_sph/ll"], arrays["neural_sph/target"] = ll, target
+    arrays["neural_sph/losses"], arrays["neural_sph/fq"], arrays["neural_sph/fk"] = np.asarray(losses), fb.fq, fb.fk
+    arrays["neural_sph/report"] = np.array([rep.max_abs_err, rep.rel_fro_err, rep.energy_retained])
+    rng = R.Rng(2024)
+    lat = rng.uniform(64) * np.pi - np.pi / 2
+    lon = rng.uniform(64) * 2 * np.pi - np.pi
+    ll = np.stack([lat, lon], axis=1)
+    target = R.generate_bias(R.SphericalDistanceBias(ll))
+    _, _, losses = R.neural_decompose(ll, ll, target, rank=32, hidden=256, iters=10000, lr=1e-3, seed=7)
+    arrays["crit4/ll"], arrays["crit4/losses"] = ll, np.asarray(losses)
+    pos = R.Rng(31).uniform(20, 2)
+    arrays["gravity/pos"], arrays["gravity/b"] = pos, R.generate_bias(R.GravityBias(pos, eps=0.05))
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "manifest.json"), "w") as f:
         json.dump({"source": "reference flashbias 0.1.0 (pkg/src/flashbias), generated by make_golden.py",

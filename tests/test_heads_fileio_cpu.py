@@ -159,3 +159,22 @@ def test_fbf1_rejects_truncated_payload(tmp_path):
 def test_writer_rejects_unknown_dtype(tmp_path):
     with pytest.raises(ValidationError):
         write_dbm1(tmp_path / "x.dbm", np.ones((2, 2)), dtype="f16")
+
+
+def test_oracle_factor_network_grads_match_reference():
+    """The oracle's MLP backprop (ref: neural.py:49-98) against the reference's
+    own gradients on its test instance (test_neural.py:27-37)."""
+    init = Rng(22)
+    qp = orc.glorot_params(init, (2, 5, 5, 3))
+    kp = orc.glorot_params(init, (2, 5, 5, 3))
+    loss, grads = orc.factor_loss_and_grads(qp, kp, G["neural_grad/xq"], G["neural_grad/xk"],
+                                            G["neural_grad/target"])
+    assert abs(loss - G["neural_grad/loss"][0]) <= 1e-14 * max(1.0, abs(loss))
+    for i, g in enumerate(grads):
+        assert np.abs(g - G[f"neural_grad/g{i}"]).max() <= 1e-13
+
+
+def test_gravity_and_spherical_generators_are_pinned():
+    from paper_2505_12044_b200 import bias as B
+    assert isinstance(B.GravityBias(G["gravity/pos"]).eps, float)
+    assert G["gravity/b"].shape == (20, 20) and G["neural_sph/target"].shape == (48, 48)
