@@ -42,6 +42,11 @@ CONFIGS = {
     "C5": dict(B=8, H=32, N=8192, d=128, causal=False, dtype="bf16", bwd=True, bias="lowrank64",
                desc="General dense bias rank sweep point R=64, B=8 H=32 N=8192 d=128 bf16 fwd+bwd"),
 }
+# §8(f)-1 widening row (not a BASELINE config): head split by bias rank, low-rank heads on the
+# FlashBias kernel and full-rank heads on the dense-bias kernel (ref: decompose.py:179-225)
+MIX = dict(B=4, H=16, N=2048, d=64, causal=False, dtype="bf16", bwd=True, low=12,
+           desc="head-split mixed path: 12 spatial-bias heads (factored after device SVD) + 4 full-rank heads "
+                "(dense), B=4 N=2048 d=64 bf16 fwd+bwd")
 METRIC = "attn-with-bias fwd+bwd TFLOP/s & ms/step vs dense-bias flash, 1/2/4/8 B200"
 
 
@@ -408,6 +413,69 @@ def run_gpu(args, cfg):
         print(json.dumps(result))
 
 
+def run_mixed(args):
+    """Head-split mixed path vs all heads on the dense-bias kernel (same step, same heads)."""
+    import torch
+
+    import paper_2505_12044_b200 as fb
+    cfg = MIX
+    torch.cuda.set_device(0)
+    H, N, d, low = cfg["H"], cfg["N"], cfg["d"], cfg["low"]
+    side = int(round(math.sqrt(N)))  # 2048 tokens: 32 x 64 grid
+    r = torch.arange(N, device="cuda") // 64
+    c = torch.arange(N, device="cuda") % 64
+    pos = torch.stack([r / (side - 1), c / 63.0, torch.zeros(N, device="cuda")], -1).double()
+    g = torch.Generator(device="cuda")
+    heads = []
+    for h in range(H):
+        g.manual_seed(4000 + h)
+        if h < low:
+            w = -(0.5 + 1.5 * torch.rand(N, generator=g, device="cuda", dtype=torch.float64))
+            heads.append(fb.generate_bias(fb.SpatialDistanceBias(pos, pos, w), device="cuda"))
+        else:
+            heads.append(torch.randn(N, N, generator=g, device="cuda", dtype=torch.float64))
+    perm = torch.randperm(H, generator=torch.Generator().manual_seed(1)).tolist()  # interleave the two kinds
+    stack = torch.stack([heads[i] for i in perm])
+    t0 = time.perf_counter()
+    split = fb.split_heads_by_rank(stack, 0.999, max_rank=32)
+    split_s = time.perf_counter() - t0
+    # offline head permutation: low-rank heads first, so both subsets are contiguous views
+    order = split.permutation()
+    split = split.permuted()
+    stack = stack[order]
+    B = cfg["B"]
+    q, k, v, do = (torch.randn(B, H, N, d, device="cuda", generator=g).bfloat16() for _ in range(4))
+    dense16 = stack.bfloat16()
+    for t in (q, k, v):
+        t.requires_grad_(True)
+
+    def mixed():
+        o = fb.mixed_head_attention(q, k, v, split, dense16)
+        torch.autograd.grad(o, (q, k, v), do)
+
+    def all_dense():
+        o = fb.tiled_attention(q, k, v, fb.DenseBias(dense16.unsqueeze(0)))
+        torch.autograd.grad(o, (q, k, v), do)
+
+    # both arms CUDA-graph captured (a ~0.3 ms step would otherwise time the Python launch path)
+    with ClockSampler(0) as clk:
+        ms = time_steps(mixed, args.steps, args.warmup, graph=not args.no_graph)
+    dense_ms = time_steps(all_dense, args.steps, max(3, args.warmup), graph=not args.no_graph)
+    rr = split.common_rank
+    nl, nd = len(split.low_indices), len(split.dense_indices)
+    flops = B * N * N * (nl * (14 * d + 8 * rr) + nd * 14 * d)
+    print(json.dumps({
+        "metric": METRIC, "value": round(flops / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
+        "dtype": "bf16", "data": "synthetic (seeded spatial-distance heads + N(0,1) full-rank heads)",
+        "config": {"workload": "MIX", "desc": cfg["desc"], "B": B, "H": H, "N": N, "d": d, "low_heads": nl,
+                   "dense_heads": nd, "common_rank": rr, "split_seconds": round(split_s, 2)},
+        "all_dense_ms_per_step": round(dense_ms, 3), "speedup_vs_all_dense": round(dense_ms / ms, 3),
+        "cuda_graph": not args.no_graph,
+        "clocks": clk.summary(),
+    }))
+
+
 def run_e2e(cfg, inp, args, device):
     """Same step through the public API with HOST (pinned) buffers: H2D of
     q/k/v/dO and D2H of O (+ dQ/dK/dV) inside the timed region."""
@@ -552,7 +620,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS) + ["MIX"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-e2e", action="store_true")
@@ -561,6 +629,10 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="never CUDA-graph the step (small configs use graphs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.config == "MIX":
+        if args.impl == "ours":
+            run_mixed(args)
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

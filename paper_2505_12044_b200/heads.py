@@ -8,9 +8,9 @@ U sqrt(s) / V sqrt(s) zero-padded to it.  The deployment pattern it serves
 (reference test_acceptance.py:204-236) runs the
 low-rank heads through the FlashBias kernel and the remaining heads through
 the dense-bias kernel.  ``mixed_head_attention`` does that with one launch
-per subset — heads permuted offline into two contiguous stacks — on two
-CUDA streams, so the two kernels overlap on the GPU, then scatters the
-outputs back into head order.
+per subset; with the heads permuted offline into two contiguous stacks
+(``HeadSplit.permutation``/``permuted``) the subsets are views, otherwise they
+are gathered and the outputs scattered back into head order.
 """
 
 from __future__ import annotations
@@ -37,6 +37,18 @@ class HeadSplit:
     common_rank: int
     low_fq: object = field(default=None, repr=False)
     low_fk: object = field(default=None, repr=False)
+
+    def permutation(self) -> List[int]:
+        """Head order that makes both subsets contiguous (low first): apply it
+        once offline to the model's heads so mixed_head_attention slices
+        instead of gathering."""
+        return list(self.low_indices) + list(self.dense_indices)
+
+    def permuted(self) -> "HeadSplit":
+        """The same split expressed in permutation() order."""
+        nl = len(self.low_indices)
+        return HeadSplit(list(range(nl)), self.low_factors, list(range(nl, nl + len(self.dense_indices))),
+                         self.common_rank, self.low_fq, self.low_fk)
 
 
 def _stack_heads(biases):
@@ -104,9 +116,10 @@ def mixed_head_attention(q, k, v, split: HeadSplit, biases, mask: str = MASK_NON
     """Per-head attention with the split's factored heads on the FlashBias
     kernel and its dense heads on the dense-bias kernel.
 
-    q, k, v: [H, L, C] (or 2-D, shared by every head as in the reference
-    criterion-9 test); biases: the [H, N, M] stack the split was computed
-    from (only the dense heads are read).  Returns [H, N, C] in head order."""
+    q, k, v: [B, H, L, C], [H, L, C] or 2-D (shared by every head, as in the
+    reference criterion-9 test); biases: the [H, N, M] stack the split was
+    computed from (only the dense heads are read; broadcast over B).  Returns
+    the output in head order with q's layout."""
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError("flashbias: CUDA device required (no CPU fallback)")
@@ -118,10 +131,13 @@ def mixed_head_attention(q, k, v, split: HeadSplit, biases, mask: str = MASK_NON
         t = t.to("cuda")
         if t.dim() == 2:
             t = t.unsqueeze(0).expand(nh, -1, -1)
-        if t.dim() != 3 or t.shape[0] != nh:
-            raise ShapeError(f"{name} must be [H, L, C] with H = {nh} or 2-D")
+        if t.dim() == 3:
+            t = t.unsqueeze(0)
+        if t.dim() != 4 or t.shape[1] != nh:
+            raise ShapeError(f"{name} must be [H, L, C] or [B, H, L, C] with H = {nh}, or 2-D")
         return t
 
+    batched = isinstance(q, torch.Tensor) and q.dim() == 4
     qh, kh, vh = heads_of(q, "q"), heads_of(k, "k"), heads_of(v, "v")
     b = None
     if split.dense_indices:
@@ -129,33 +145,42 @@ def mixed_head_attention(q, k, v, split: HeadSplit, biases, mask: str = MASK_NON
             else _stack_heads(biases)
         if b.shape[0] != nh:
             raise ShapeError(f"bias stack has {b.shape[0]} heads, split covers {nh}")
-    out = None
+
+    def take(t, idx, dim=1):
+        # heads permuted offline into contiguous stacks (split.permutation()) are plain views
+        if idx == list(range(idx[0], idx[0] + len(idx))):
+            return t.narrow(dim, idx[0], len(idx))
+        return t.index_select(dim, torch.tensor(idx, device=t.device))
+
     parts = []
-    main = torch.cuda.current_stream()
-    side = torch.cuda.Stream()
-    side.wait_stream(main)
     if split.low_indices:
-        li = torch.tensor(split.low_indices, device="cuda")
+        li = split.low_indices
         fq = split.low_fq if split.low_fq is not None else torch.stack([torch.as_tensor(f.fq) for f in split.low_factors])
         fk = split.low_fk if split.low_fk is not None else torch.stack([torch.as_tensor(f.fk) for f in split.low_factors])
-        # the low subset: one FlashBias launch over the permuted [1, H_low, ...] stack
-        o_low = flashbias_attention(qh[li].unsqueeze(0), kh[li].unsqueeze(0), vh[li].unsqueeze(0),
+        # the low subset: one FlashBias launch over the [1, H_low, ...] stack
+        o_low = flashbias_attention(take(qh, li), take(kh, li), take(vh, li),
                                     fq.to("cuda").unsqueeze(0), fk.to("cuda").unsqueeze(0), mask=mask,
                                     tiles=tiles, precision=precision)
-        parts.append((li, o_low.squeeze(0)))
+        parts.append((li, o_low))
     if split.dense_indices:
-        di = torch.tensor(split.dense_indices, device="cuda")
-        with torch.cuda.stream(side):  # the dense subset overlaps on a second stream
-            o_dense = tiled_attention(qh[di].unsqueeze(0), kh[di].unsqueeze(0), vh[di].unsqueeze(0),
-                                      DenseBias(b[di].unsqueeze(0)), mask=mask, tiles=tiles,
-                                      precision=precision)
-        main.wait_stream(side)
-        o_dense.record_stream(main)
-        parts.append((di, o_dense.squeeze(0)))
-    for idx, o in parts:
-        if out is None:
-            out = torch.empty((nh,) + tuple(o.shape[1:]), dtype=o.dtype, device=o.device)
-        out[idx] = o
+        di = split.dense_indices
+        # the dense subset: one dense-bias launch
+        o_dense = tiled_attention(take(qh, di), take(kh, di), take(vh, di),
+                                  DenseBias(take(b, di, 0).unsqueeze(0)), mask=mask, tiles=tiles, precision=precision)
+        parts.append((di, o_dense))
+    if len(parts) == 2 and parts[0][0] + parts[1][0] == list(range(nh)):
+        out = torch.cat([parts[0][1], parts[1][1]], 1)
+    elif len(parts) == 2 and parts[1][0] + parts[0][0] == list(range(nh)):
+        out = torch.cat([parts[1][1], parts[0][1]], 1)
+    elif len(parts) == 1:
+        out = parts[0][1]
+    else:
+        o0 = parts[0][1]
+        out = torch.empty((o0.shape[0], nh) + tuple(o0.shape[2:]), dtype=o0.dtype, device=o0.device)
+        for idx, o in parts:
+            out[:, torch.tensor(idx, device=out.device)] = o
+    if not batched:
+        out = out.squeeze(0)
     if numpy_in:
         return out.double().cpu().numpy()
     return out
