@@ -183,7 +183,7 @@ def step_fn(cfg, inp, mode: str):
         q.requires_grad_(True)
         k.requires_grad_(True)
         v.requires_grad_(True)
-        if cfg["bias"] == "spatial" and mode == "flashbias":
+        if cfg["bias"] == "spatial" and mode == "flashbias" and not cfg.get("static"):
             inp["fq"].requires_grad_(True)
             inp["fk"].requires_grad_(True)
 
@@ -664,13 +664,18 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-graph", action="store_true", help="never CUDA-graph the step (small configs use graphs)")
+    ap.add_argument("--static-factors", action="store_true",
+                    help="C2: treat the spatial factors as a fixed bias (no factor gradients), like the dense arm")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.config == "MIX":
         if args.impl == "ours":
             run_mixed(args)
         return
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.static_factors:
+        cfg["static"] = True
+        cfg["desc"] += " [static factors: no factor gradients]"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int c = 0; c < 64; ++c) {
           const float2 e2 = ffma2(make_float2(x[2 * c], x[2 * c + 1]), mul, neg);
           // FB_POLY_NUM pairs in 8 go through the FMA-pipe polynomial, the rest through MUFU
-          const float2 p2 = poly_pair_fwd(c) ? ex2_poly2(e2) : make_float2(ex2(e2.x), ex2(e2.y));
+          const float2 p2 = poly_pair_fwd<D>(c) ? ex2_poly2(e2) : make_float2(ex2(e2.x), ex2(e2.y));
           acc[c & 3] = fadd2(acc[c & 3], p2);
           pk[c] = pack2<BF16>(p2.x, p2.y);
           if (c == kSplitPairs - 1) {  // first 3/4 of P -> TMEM, release PV K-steps 0..5

@@ -340,11 +340,19 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 #define FB_POLY_NUM 0
 #endif
 __host__ __device__ constexpr bool poly_pair(int c) { return ((c & 7) * FB_POLY_NUM) % 8 < FB_POLY_NUM; }
-// forward softmax (MUFU-heavy: 16384 ex2 per 128x128 tile against ~1088 tensor cycles)
+// forward softmax (MUFU-heavy: 16384 ex2 per 128x128 tile against ~1088 tensor cycles at d=128;
+// at d <= 64 the tile's MMAs take ~750 cycles, so the softmax is MUFU-bound and has its own knob)
 #ifndef FB_POLY_NUM_FWD
 #define FB_POLY_NUM_FWD 0
 #endif
-__host__ __device__ constexpr bool poly_pair_fwd(int c) { return ((c & 7) * FB_POLY_NUM_FWD) % 8 < FB_POLY_NUM_FWD; }
+#ifndef FB_POLY_NUM_FWD_SMALL_D
+#define FB_POLY_NUM_FWD_SMALL_D 0
+#endif
+template <int D>
+__host__ __device__ constexpr bool poly_pair_fwd(int c) {
+  return D >= 128 ? ((c & 7) * FB_POLY_NUM_FWD) % 8 < FB_POLY_NUM_FWD
+                  : ((c & 7) * FB_POLY_NUM_FWD_SMALL_D) % 8 < FB_POLY_NUM_FWD_SMALL_D;
+}
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
