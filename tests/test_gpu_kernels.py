@@ -162,3 +162,38 @@ def test_bwd_ragged():
 @pytest.mark.parametrize("causal", [False, True])
 def test_bwd_dense(causal):
     _bwd_case(1, 2, 256, 256, 128, 0, causal, dense=True)
+
+
+def _bwd_static_case(B, H, N, M, D, R, causal, seed=0, factor_batch=1):
+    """Static (non-learnable) factors: d=128 with Rpad <= 16 runs the 128x128-tile
+    backward (fb_bwd_t128_sm100.cu); dq/dk/dv checked against torch fp64."""
+    q, k, v = _qkv(B, H, N, M, D, torch.bfloat16, seed=seed)
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    g = torch.Generator(device="cuda").manual_seed(seed + 11)
+    fq = torch.randn(factor_batch, H, N, R, device="cuda", generator=g) * 0.7
+    fk = torch.randn(factor_batch, H, M, R, device="cuda", generator=g) * 0.7
+    do = torch.randn(B, H, N, D, device="cuda", generator=g).bfloat16()
+    mask = "causal" if causal else "none"
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask=mask)
+    out.backward(do)
+    ref_leaves = [t.detach().double().requires_grad_(True) for t in (q, k, v)]
+    ref = ref_attention(*ref_leaves, fq.double(), fk.double(), causal=causal)
+    ref.backward(do.double())
+    for name, got, r_ in zip(["dq", "dk", "dv"], (q.grad, k.grad, v.grad), ref_leaves):
+        e = relerr(got, r_.grad)
+        assert e < BF16_TOL, f"{name}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("B,H,N,M,R,causal,fb_", [
+    (2, 2, 384, 384, 2, True, 1),      # ALiBi-like rank 2 -> 3-way split, 1 panel; batch-broadcast factors
+    (1, 2, 200, 200, 2, True, 1),      # ragged causal (N % 128 != 0)
+    (1, 2, 150, 333, 4, False, 1),     # N != M, ragged both sides
+    (2, 3, 257, 129, 2, False, 2),     # per-batch factors, 3 heads
+    (1, 1, 640, 640, 0, True, 1),      # no factors (Rpad 0 instance)
+])
+def test_bwd_t128_static_factors(B, H, N, M, R, causal, fb_):
+    if R == 0:
+        _bwd_case(B, H, N, M, 128, 0, causal, seed=3)
+    else:
+        _bwd_static_case(B, H, N, M, 128, R, causal, seed=B * 10 + R, factor_batch=fb_)
