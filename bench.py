@@ -202,11 +202,14 @@ def step_fn(cfg, inp, mode: str):
     return run
 
 
-def time_steps(fn, steps: int, warmup: int, dist=None, graph: bool = False):
+def time_steps(fn, steps: int, warmup: int, dist=None, graph: bool = False, flush: bool = False):
     """CUDA-event timing of `steps` calls after `warmup` untimed ones, barrier +
     synchronize on both sides.  graph=True captures one step in a CUDA graph
     (after warm-up) and times its replays — for the microsecond-scale configs
-    whose step would otherwise be bound by Python launch overhead."""
+    whose step would otherwise be bound by Python launch overhead.
+    flush=True writes a 256 MB buffer (> the 126 MB L2) before every step,
+    outside the events that bracket that step, so small configs are not timed
+    from a warm L2; the per-step event intervals are summed."""
     import torch
     for _ in range(warmup):
         fn()
@@ -223,19 +226,31 @@ def time_steps(fn, steps: int, warmup: int, dist=None, graph: bool = False):
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
         fn = g.replay
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if flush else None
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
-    for _ in range(steps):
-        fn()
-    stop.record()
-    torch.cuda.synchronize()
+    if flush:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in evs:
+            scratch.fill_(1)
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize()
+        total = sum(a.elapsed_time(b) for a, b in evs)
+    else:
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        for _ in range(steps):
+            fn()
+        stop.record()
+        torch.cuda.synchronize()
+        total = start.elapsed_time(stop)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    return start.elapsed_time(stop) / steps
+    return total / steps
 
 
 def kernel_breakdown(cfg, inp, reps: int = 3):
@@ -302,6 +317,8 @@ def run_gpu(args, cfg):
 
     fn = step_fn(cfg, inp, "flashbias")
     use_graph = alg_flops(cfg, total_bh) < 20e9 and not args.no_graph
+    in_bytes = cfg["N"] * cfg["d"] * (2 if cfg["dtype"] == "bf16" else 4) * 4 * n_loc
+    flush = in_bytes < 2 * 126e6  # inputs not much larger than L2: flush before every timed step
     fn()  # one eager step: count this library's kernel launches per step
     torch.cuda.synchronize()
     lib.fb_launch_count(1)
@@ -309,7 +326,7 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
     launches_per_step = int(lib.fb_launch_count(1))
     with ClockSampler(local) as clk:
-        ms = time_steps(fn, args.steps, args.warmup, dist, graph=use_graph)
+        ms = time_steps(fn, args.steps, args.warmup, dist, graph=use_graph, flush=flush)
     launches_timed = launches_per_step * args.steps
     if dist is not None:
         t = torch.tensor([ms], device=device)
@@ -347,7 +364,8 @@ def run_gpu(args, cfg):
                                                  _lib.ref(D(dense)), _lib.stream_ptr(device)))
         inp["dense"] = dense
         dfn = step_fn(cfg, inp, "dense")
-        dense_ms = time_steps(dfn, max(1, args.steps), max(1, min(args.warmup, 2)), dist, graph=use_graph)
+        dense_ms = time_steps(dfn, max(1, args.steps), max(1, min(args.warmup, 2)), dist, graph=use_graph,
+                              flush=flush)
         if dist is not None:
             t = torch.tensor([dense_ms], device=device)
             dist.all_reduce(t, op=dist_mod.ReduceOp.MAX)
@@ -392,8 +410,8 @@ def run_gpu(args, cfg):
         "config": {"workload": args.config, "desc": cfg["desc"], "B": cfg["B"], "H": cfg["H"], "N": cfg["N"],
                    "M": cfg["N"], "d": cfg["d"], "R": logical_rank(cfg), "causal": cfg["causal"],
                    "bwd": cfg["bwd"], "parallelism": f"bh-shard{world}",
-                   "l2": "inputs larger than L2 (no flush needed)" if cfg["N"] * cfg["d"] * 2 * n_loc > 126e6
-                   else "inputs smaller than L2 (repeated steps hit L2)"},
+                   "l2": ("L2 flushed (256 MB write) before every timed step, outside its events" if flush
+                          else "inputs larger than L2 (no flush needed)")},
         "gather_ms_per_step": None if gather_ms is None else round(gather_ms, 3),
         "ms_per_step_with_gather": None if gather_ms is None else round(ms + gather_ms, 3),
         "dense_bias_ms_per_step": None if dense_ms is None else round(dense_ms, 3),
@@ -459,8 +477,8 @@ def run_mixed(args):
 
     # both arms CUDA-graph captured (a ~0.3 ms step would otherwise time the Python launch path)
     with ClockSampler(0) as clk:
-        ms = time_steps(mixed, args.steps, args.warmup, graph=not args.no_graph)
-    dense_ms = time_steps(all_dense, args.steps, max(3, args.warmup), graph=not args.no_graph)
+        ms = time_steps(mixed, args.steps, args.warmup, graph=not args.no_graph, flush=True)
+    dense_ms = time_steps(all_dense, args.steps, max(3, args.warmup), graph=not args.no_graph, flush=True)
     rr = split.common_rank
     nl, nd = len(split.low_indices), len(split.dense_indices)
     flops = B * N * N * (nl * (14 * d + 8 * rr) + nd * 14 * d)
@@ -471,7 +489,7 @@ def run_mixed(args):
         "config": {"workload": "MIX", "desc": cfg["desc"], "B": B, "H": H, "N": N, "d": d, "low_heads": nl,
                    "dense_heads": nd, "common_rank": rr, "split_seconds": round(split_s, 2)},
         "all_dense_ms_per_step": round(dense_ms, 3), "speedup_vs_all_dense": round(dense_ms / ms, 3),
-        "cuda_graph": not args.no_graph,
+        "cuda_graph": not args.no_graph, "l2": "L2 flushed (256 MB write) before every timed step, outside its events",
         "clocks": clk.summary(),
     }))
 
