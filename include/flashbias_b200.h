@@ -115,6 +115,18 @@ int fb_prepare_factors(const fb_tensor* f, int side, int split, float premul,
 int64_t fb_factor_rpad(int64_t rank, int split);
 int64_t fb_factor_cols(int64_t rank, int split);
 
+/* Fused neural-factor prologue (replaces evaluating the reference's factor
+ * networks, neural.py:44-47 / FactorNetworks.factors 76-77, and then
+ * fb_prepare_factors): y = tanh(tanh(x W1 + b1) W2 + b2) W3 + b3 per token,
+ * written straight into the split panel layout of fb_prepare_factors.
+ *   x  : f32 [1,1,L,in] (in <= 8), w1 [1,1,in,h], b1 [1,1,1,h], w2 [1,1,h,h],
+ *        b2 [1,1,1,h], w3 [1,1,h,R], b3 [1,1,1,R] (fp32, row-major, h <= 1024, R <= 128)
+ *   out: bf16|f16 [1,1,L,Rpad]; factors: nullable fp32 [1,1,L,R] copy of y. */
+int fb_mlp_factor_panels(const fb_tensor* x, const fb_tensor* w1, const fb_tensor* b1,
+                         const fb_tensor* w2, const fb_tensor* b2, const fb_tensor* w3,
+                         const fb_tensor* b3, int side, int split, float premul,
+                         fb_tensor* out, fb_tensor* factors, void* stream);
+
 /* Inverse of fb_prepare_factors for gradients: d(logical f)[b,h,l,r] =
  * postmul * sum over the split columns of rank r whose *partner* part is the
  * leading one, reduced over the batch dim when the factor was broadcast

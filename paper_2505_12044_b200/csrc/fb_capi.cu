@@ -491,6 +491,45 @@ int fb_prepare_factors(const fb_tensor* f, int side, int split, float premul, fb
   return e == cudaSuccess ? FB_OK : cuda_fail(e, "prepare_factors");
 }
 
+int fb_mlp_factor_panels(const fb_tensor* x, const fb_tensor* w1, const fb_tensor* b1, const fb_tensor* w2,
+                         const fb_tensor* b2, const fb_tensor* w3, const fb_tensor* b3, int side, int split,
+                         float premul, fb_tensor* out, fb_tensor* factors, void* stream) {
+  if (!x || !w1 || !b1 || !w2 || !b2 || !w3 || !b3 || !out) return fail(FB_EVALUE, "null tensor");
+  for (const fb_tensor* t : {x, w1, b1, w2, b2, w3, b3})
+    if (t->dtype != FB_F32) return fail(FB_EVALUE, "MLP inputs and weights are fp32");
+  if (split < 1 || split > 3) return fail(FB_EVALUE, "split must be 1, 2 or 3");
+  if (side != 0 && side != 1) return fail(FB_EVALUE, "side must be 0 (query) or 1 (key)");
+  if (out->dtype != FB_BF16 && out->dtype != FB_F16) return fail(FB_EVALUE, "panels are bf16/f16");
+  const int64_t L = x->shape[2], in = x->shape[3], hid = w1->shape[3], R = w3->shape[3];
+  if (in < 1 || in > 8) return fail(FB_ECONFIG, "MLP input dim must be 1..8");
+  if (hid < 1 || hid > 1024 || R < 1 || R > 128) return fail(FB_ECONFIG, "hidden <= 1024 and rank <= 128");
+  if (w1->shape[2] != in || w2->shape[2] != hid || w2->shape[3] != hid || w3->shape[2] != hid ||
+      b1->shape[3] != hid || b2->shape[3] != hid || b3->shape[3] != R)
+    return fail(FB_ESHAPE, "MLP weight shapes do not chain: [in,h] [h,h] [h,R]");
+  for (const fb_tensor* t : {w1, b1, w2, b2, w3, b3})
+    if (t->stride[3] != 1 || (t->shape[2] > 1 && t->stride[2] != t->shape[3]))
+      return fail(FB_ESHAPE, "MLP weights must be contiguous row-major");
+  if (x->stride[3] != 1) return fail(FB_ESHAPE, "x rows must be contiguous");
+  if (out->shape[2] != L || out->shape[3] < fb_factor_cols(R, split) || out->stride[3] != 1)
+    return fail(FB_ESHAPE, "panel must be [L, >= fb_factor_cols(R, split)] with contiguous rows");
+  if (factors && (factors->dtype != FB_F32 || factors->shape[2] != L || factors->shape[3] != R ||
+                  factors->stride[3] != 1 || factors->stride[2] != R))
+    return fail(FB_ESHAPE, "factors output must be contiguous fp32 [L, R]");
+  MlpParams p{};
+  p.x = static_cast<const float*>(x->data); p.x_stride = x->stride[2];
+  p.L = (int)L; p.in_dim = (int)in; p.hidden = (int)hid; p.R = (int)R;
+  p.w1 = static_cast<const float*>(w1->data); p.b1 = static_cast<const float*>(b1->data);
+  p.w2 = static_cast<const float*>(w2->data); p.b2 = static_cast<const float*>(b2->data);
+  p.w3 = static_cast<const float*>(w3->data); p.b3 = static_cast<const float*>(b3->data);
+  p.side = side; p.split = split; p.rpad = (int)out->shape[3]; p.out_dtype = out->dtype;
+  p.premul = side == 0 ? premul : 1.0f;
+  p.out = out->data; p.out_stride = out->stride[2];
+  p.factors_out = factors ? static_cast<float*>(factors->data) : nullptr;
+  cudaError_t e = launch_mlp_panels(p, reinterpret_cast<cudaStream_t>(stream));
+  note_launch();
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "mlp_factor_panels");
+}
+
 int fb_fold_factor_grads(const fb_tensor* dpanel, int side, int split, float postmul, fb_tensor* out, void* stream) {
   if (!dpanel || !out) return fail(FB_EVALUE, "null tensor");
   if (split < 1 || split > 3) return fail(FB_EVALUE, "split must be 1, 2 or 3");

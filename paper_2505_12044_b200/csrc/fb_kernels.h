@@ -114,6 +114,18 @@ cudaError_t launch_bwd_preprocess(const Tensor4& o, const Tensor4& dout, const T
 
 int factor_pairs(int split);
 
+// ----- fused neural-factor prologue (fb_neural.cu)
+struct MlpParams {
+  const float* x; int64_t x_stride;  // [L, in_dim] fp32 coordinates
+  int L, in_dim, hidden, R;
+  const float *w1, *b1, *w2, *b2, *w3, *b3;  // row-major [in,h] [h] [h,h] [h] [h,R] [R] fp32
+  int side, split, rpad, out_dtype;  // panel layout of fb_prepare_factors
+  float premul;
+  void* out; int64_t out_stride;     // [L, rpad] bf16/f16 panel
+  float* factors_out;                // nullable [L, R] fp32
+};
+cudaError_t launch_mlp_panels(const MlpParams& p, cudaStream_t s);
+
 // debug timeline trace target (fb_debug_set_trace)
 void trace_target(unsigned long long** buf, int* cta);
 

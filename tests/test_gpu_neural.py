@@ -103,3 +103,29 @@ def test_reference_neural_error_cases():
     b = fb.neural_decompose(G["neural_fit/xq"][:6], G["neural_fit/xq"][:5], G["neural_fit/target"][:6, :5],
                             rank=2, hidden=8, iters=40, seed=9)
     assert np.array_equal(a[0].fq, b[0].fq) and a[2] == b[2]  # deterministic
+
+
+@pytest.mark.parametrize("hidden,rank,split", [(32, 8, 2), (256, 32, 1), (64, 4, 3)])
+def test_fused_mlp_prologue_matches_two_step_path(hidden, rank, split):
+    """fb_mlp_factor_panels == evaluate the networks, then fb_prepare_factors."""
+    from paper_2505_12044_b200 import attention as A
+    rng = fb.Rng(91)
+    xq, xk = rng.uniform(300, 2) * 2 - 1, rng.uniform(260, 2) * 2 - 1
+    nets = fb.FactorNetworks.init(fb.Rng(5), 2, hidden, rank)
+    uq, uk, f32q, f32k = nets.panels(xq, xk, premul=8.0, split=split, with_factors=True)
+    fq, fk = nets.factors(xq, xk)  # float64 reference evaluation
+    assert (f32q.double() - fq).abs().max().item() <= 1e-5 * max(1.0, fq.abs().max().item())
+    assert (f32k.double() - fk).abs().max().item() <= 1e-5 * max(1.0, fk.abs().max().item())
+    rq, rk = A.prepare_factor_panels(f32q, f32k, 8.0, split, torch.bfloat16)
+    assert torch.equal(uq, rq) and torch.equal(uk, rk)
+
+
+def test_neural_flashbias_attention_vs_oracle():
+    ll, target = G["neural_sph/ll"], G["neural_sph/target"]
+    f, nets, _ = fb.neural_decompose(ll, ll, target, rank=8, hidden=32, iters=100, seed=3)
+    torch.manual_seed(4)
+    q, k, v = (torch.randn(2, 3, 48, 64, device="cuda").bfloat16() for _ in range(3))
+    for mask in ("none", "causal"):
+        o = fb.neural_flashbias_attention(q, k, v, nets, ll, ll, mask=mask)
+        want = orc.flashbias_attention(*(t.double().cpu().numpy() for t in (q, k, v)), f.fq, f.fk, mask=mask)
+        assert orc.rel_max_err(o.double().cpu().numpy(), want) <= 2e-2
