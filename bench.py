@@ -401,7 +401,7 @@ def run_gpu(args, cfg):
             "factor_split": kb["split"], "factor_rpad": kb["rpad"],
         }
 
-    e2e = run_e2e(cfg, inp, args, device) if not args.skip_e2e else None
+    e2e = run_e2e(cfg, inp, args, device, dist=dist, total_bh=total_bh) if not args.skip_e2e else None
     result = {
         "metric": METRIC, "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
@@ -494,7 +494,7 @@ def run_mixed(args):
     }))
 
 
-def run_e2e(cfg, inp, args, device, chunks: int = 8):
+def run_e2e(cfg, inp, args, device, chunks: int = 8, dist=None, total_bh=None):
     """Same step through the public API with HOST (pinned) buffers: H2D of
     q/k/v/dO and D2H of O (+ dQ/dK/dV) inside the timed region.
 
@@ -557,10 +557,20 @@ def run_e2e(cfg, inp, args, device, chunks: int = 8):
         comp.wait_stream(s_out)  # the step ends when the last D2H lands
 
     steps = max(1, min(args.steps, 3))
-    ms = time_steps(step, steps, 1)
-    flops = alg_flops(cfg, inp["q"].shape[0] * inp["q"].shape[1])
+    ms = time_steps(step, steps, 1, dist)
+    world = 1
+    if dist is not None:  # whole job: every rank moves its own heads over its own PCIe link; max over ranks
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+        world = dist.get_world_size()
+        tb = torch.tensor([h2d, d2h], dtype=torch.float64, device=device)
+        dist.all_reduce(tb)
+        h2d, d2h = int(tb[0]), int(tb[1])
+    flops = alg_flops(cfg, total_bh if total_bh is not None else inp["q"].shape[0] * inp["q"].shape[1])
     return {"value": round(flops / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s", "ms_per_step": round(ms, 2),
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "head_chunks": chunks,
+            "ranks": world,
             "path": "flashbias_attention (public API) on head slices of pinned host tensors, autograd backward; "
                     "H2D / compute / D2H software-pipelined over three streams"}
 
