@@ -492,8 +492,185 @@ __global__ void __launch_bounds__(128) fwd_simt_f32_kernel(const SimtParams p) {
   }
 }
 
+// Register-tiled SIMT forward (same numerics as fwd_simt_f32_kernel: fp32 FMA
+// q.k, fp64 factor / bias terms and running max, expf of the fp32 difference):
+// CTA = 64 query rows x 256 threads (16 x 16), KV blocks of 64 keys; thread
+// (ty, tx) owns rows 4ty..4ty+3 x keys 4tx..4tx+3 of S and rows 4ty.. x head
+// columns CPT*tx.. of O.  Q^T / K^T tiles are stored channel-major in shared
+// memory so every channel step is two float4 loads feeding 16 FMAs; P goes
+// through shared memory to the P.V product.
+template <int D>
+__global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p) {
+  constexpr int BM = 64, BN = 64, CPT = D / 16;
+  extern __shared__ float sm[];
+  const int DK = D + p.R;
+  float* sQ = sm;                  // [DK][BM]
+  float* sK = sQ + DK * BM;        // [DK][BN]
+  float* sV = sK + DK * BN;        // [BN][D]
+  float* sP = sV + BN * D;         // [BM][BN + 4]
+  constexpr int PST = BN + 4;
+  const int b = blockIdx.z, h = blockIdx.y;
+  const int q0 = blockIdx.x * BM;
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  for (int idx = t; idx < BM * DK; idx += 256) {
+    const int r = idx / DK, c = idx % DK, row = q0 + r;
+    float v = 0.f;
+    if (row < p.N) {
+      if (c < D) v = p.q[b * p.q_sb + h * p.q_sh + static_cast<int64_t>(row) * p.q_sn + c];
+      else v = p.uq[b * p.uq_sb + h * p.uq_sh + static_cast<int64_t>(row) * p.uq_sn + (c - D)];
+    }
+    sQ[c * BM + r] = v;
+  }
+  double m_run[4];
+  float l_run[4], acc[4][CPT];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m_run[i] = -INFINITY;
+    l_run[i] = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[i][c] = 0.f;
+  }
+  const int kv_end = p.causal ? min(p.M, q0 + BM) : p.M;
+  for (int kv0 = 0; kv0 < kv_end; kv0 += BN) {
+    __syncthreads();  // previous block's sK / sV / sP fully consumed
+    for (int idx = t; idx < BN * DK; idx += 256) {
+      const int r = idx / DK, c = idx % DK, j = kv0 + r;
+      float v = 0.f;
+      if (j < p.M) {
+        if (c < D) v = p.k[b * p.k_sb + h * p.k_sh + static_cast<int64_t>(j) * p.k_sn + c];
+        else v = p.uk[b * p.uk_sb + h * p.uk_sh + static_cast<int64_t>(j) * p.uk_sn + (c - D)];
+      }
+      sK[c * BN + r] = v;
+    }
+    for (int idx = t; idx < BN * D; idx += 256) {
+      const int r = idx / D, c = idx % D, j = kv0 + r;
+      sV[idx] = j < p.M ? p.v[b * p.v_sb + h * p.v_sh + static_cast<int64_t>(j) * p.v_sn + c] : 0.f;
+    }
+    __syncthreads();
+    float s[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s[i][k] = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < D; ++c) {
+      const float4 a = *reinterpret_cast<const float4*>(sQ + c * BM + 4 * ty);
+      const float4 kk = *reinterpret_cast<const float4*>(sK + c * BN + 4 * tx);
+      const float av[4] = {a.x, a.y, a.z, a.w}, kv[4] = {kk.x, kk.y, kk.z, kk.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s[i][k] = fmaf(av[i], kv[k], s[i][k]);
+    }
+    double su[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) su[i][k] = 0.0;
+    for (int c = D; c < DK; ++c) {
+      const float4 a = *reinterpret_cast<const float4*>(sQ + c * BM + 4 * ty);
+      const float4 kk = *reinterpret_cast<const float4*>(sK + c * BN + 4 * tx);
+      const double av[4] = {a.x, a.y, a.z, a.w}, kv[4] = {kk.x, kk.y, kk.z, kk.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) su[i][k] = fma(av[i], kv[k], su[i][k]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = q0 + 4 * ty + i;
+      double sd[4];
+      double mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = kv0 + 4 * tx + k;
+        double v = (static_cast<double>(s[i][k]) + su[i][k]) * static_cast<double>(p.scale);
+        if (p.bias && j < p.M && row < p.N)
+          v += p.bias[b * p.bias_sb + h * p.bias_sh + static_cast<int64_t>(row) * p.bias_sn + j];
+        if (j >= p.M || (p.causal && j > row)) v = -INFINITY;
+        sd[k] = v;
+        mx = fmax(mx, v);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const double m_new = fmax(m_run[i], mx);
+      float pk[4] = {0.f, 0.f, 0.f, 0.f};
+      float alpha = 1.f;
+      if (m_new != -INFINITY) {
+        alpha = expf(static_cast<float>(m_run[i] - m_new));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pk[k] = expf(static_cast<float>(sd[k] - m_new));
+        m_run[i] = m_new;
+      }
+      float ps = (pk[0] + pk[1]) + (pk[2] + pk[3]);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      l_run[i] = l_run[i] * alpha + ps;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) acc[i][c] *= alpha;
+      *reinterpret_cast<float4*>(sP + (4 * ty + i) * PST + 4 * tx) = make_float4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int j = 0; j < BN; ++j) {
+      float pv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pv[i] = sP[(4 * ty + i) * PST + j];
+      float vv[CPT];
+      if constexpr (CPT >= 4) {
+#pragma unroll
+        for (int c4 = 0; c4 < CPT; c4 += 4) {
+          const float4 w = *reinterpret_cast<const float4*>(sV + j * D + CPT * tx + c4);
+          vv[c4] = w.x; vv[c4 + 1] = w.y; vv[c4 + 2] = w.z; vv[c4 + 3] = w.w;
+        }
+      } else {
+        const float2 w = *reinterpret_cast<const float2*>(sV + j * D + CPT * tx);
+        vv[0] = w.x; vv[1] = w.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[i][c] = fmaf(pv[i], vv[c], acc[i][c]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = q0 + 4 * ty + i;
+    if (row >= p.N) continue;
+    const float inv = l_run[i] > 0.f ? 1.0f / l_run[i] : 0.f;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+      p.o[b * p.o_sb + h * p.o_sh + static_cast<int64_t>(row) * p.o_sn + CPT * tx + c] = acc[i][c] * inv;
+    if (p.lse && tx == 0)
+      p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + row] =
+          static_cast<float>(m_run[i] + log(static_cast<double>(l_run[i])));
+  }
+}
+
+template <int D>
+static cudaError_t launch_simt_tiled(const SimtParams& p, cudaStream_t s) {
+  const int DK = D + p.R;
+  const size_t smem = sizeof(float) * (static_cast<size_t>(DK) * 64 * 2 + 64 * D + 64 * 68);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(fwd_simt_tiled_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((p.N + 63) / 64, p.H, p.B);
+  fwd_simt_tiled_kernel<D><<<grid, 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s) {
   const int DK = p.D + p.R;
+  if (DK <= 256 && (p.D == 32 || p.D == 64 || p.D == 128)) {
+    cudaError_t e = p.D == 32 ? launch_simt_tiled<32>(p, s)
+                    : p.D == 64 ? launch_simt_tiled<64>(p, s) : launch_simt_tiled<128>(p, s);
+    note_launch();
+    return e;
+  }
   const size_t smem = sizeof(float) * (kSimtRows * DK + kSimtKv * (DK | 1) + kSimtKv * p.D);
   static bool attr = false;
   if (!attr) {
