@@ -40,7 +40,8 @@
 #define T128_REG_OT 72
 #endif
 #ifndef T128_DRAIN_MODE
-#define T128_DRAIN_MODE 0  // 0 = TMA reduce-add from a swizzled smem stage, 3 = red.global.add.v4.f32 after a
+#define T128_DRAIN_MODE 0  // 0 = TMA reduce-add from a swizzled smem stage (4 = per-warp 2 KB boxes, no
+                           // cross-warp barriers: measured equal), 3 = red.global.add.v4.f32 after a
                            // per-warp smem transpose (measured C3 bwd 25.1-25.4 ms vs 23.1 for mode 0);
                            // experiments: 1 = TMA store (wrong), 2 = no global write
 #endif
@@ -466,6 +467,49 @@ __global__ void __launch_bounds__(512, 1)
       }
       if (leader) trace(p.trace, p.trace_cta, 20, j);
     }
+#elif T128_DRAIN_MODE == 4
+    // Per-warp staging, no cross-warp barriers: warp w stages its 32 head-dim
+    // rows x 16 queries (2 KB, SW64) and its elected lane issues that box's
+    // reduce-add; two 2 KB stages per warp.
+    uint8_t* wst = reinterpret_cast<uint8_t*>(dq_stage) + (warp & 3) * 4096;
+    const int wrow0 = (warp & 3) * 32;
+    int chunk = 0;
+    for (int j = 0; j < nblk; ++j) {
+      const int q0 = (i_start + j) * 128;
+      mbar_wait(&bars->dq_full, j & 1);
+      tc_fence_after();
+      if (leader) trace(p.trace, p.trace_cta, 19, j);
+      uint32_t v[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        tmem_ld32(tmem + lane_off + T_DP + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars->dq_free);
+      const float sc = p.scale;
+#pragma unroll
+      for (int c = 0; c < 8; ++c, ++chunk) {
+        uint8_t* stg = wst + (chunk & 1) * 2048;
+        if (lane == 0) t128_wait_read<1>();
+        __syncwarp();
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const int e = 16 * c + 4 * c4;
+          *reinterpret_cast<float4*>(stg + lane * 64 + ((c4 ^ ((lane >> 1) & 3)) << 4)) =
+              make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
+                          __uint_as_float(v[e + 3]) * sc);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          t128_reduce_add(&tm_dqacc, stg, q0 + 16 * c, wrow0, h, b);
+          t128_bulk_commit();
+        }
+      }
+      if (leader) trace(p.trace, p.trace_cta, 20, j);
+    }
+    if (lane == 0) t128_wait_all();
 #else
     int chunk = 0;
     for (int j = 0; j < nblk; ++j) {
@@ -580,7 +624,8 @@ cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, 
   return cudaGetLastError();
 }
 
-int bwd_t128_qchunk() { return T128_QCHUNK; }
+int bwd_t128_qchunk() { return T128_DRAIN_MODE == 4 ? 16 : T128_QCHUNK; }
+int bwd_t128_box_rows() { return T128_DRAIN_MODE == 4 ? 32 : 128; }
 
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads) {
   return d == 128 && rp <= 1 && !dense && !factor_grads;

@@ -432,7 +432,7 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
       tt.stride[3] = 1; tt.stride[2] = n4; tt.stride[1] = n4 * D; tt.stride[0] = n4 * D * H;
       tt.dtype = FB_F32;
       CUtensorMap macc_t;
-      if ((rc = make_map(&macc_t, &tt, bwd_t128_qchunk(), 128, bwd_t128_qchunk() * 4, "dq_acc_t"))) return rc;
+      if ((rc = make_map(&macc_t, &tt, bwd_t128_qchunk(), bwd_t128_box_rows(), bwd_t128_qchunk() * 4, "dq_acc_t"))) return rc;
       e = cudaMemsetAsync(acc, 0, (size_t)B * H * n4 * D * sizeof(float), s);
       if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
       p.dq_acc = acc;
