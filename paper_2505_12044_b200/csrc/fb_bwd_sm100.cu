@@ -610,13 +610,12 @@ static cudaError_t launch_bwd_t(const BwdMaps& m, const BwdParams& p, cudaStream
   using Cfg = BwdCfg<D, RP, DENSE>;
   auto kdkv = fb_bwd_dkv_kernel<D, RP, DENSE, BF16, FGRAD>;
   auto kdq = fb_bwd_dq_kernel<D, RP, DENSE, BF16, FGRAD>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kdkv, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kKVSmem);
+  static std::atomic<uint64_t> attr_kv{0}, attr_q{0};
+  {
+    cudaError_t e = smem_attr_once(attr_kv, reinterpret_cast<const void*>(kdkv), Cfg::kKVSmem);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kdq, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kQSmem);
+    e = smem_attr_once(attr_q, reinterpret_cast<const void*>(kdq), Cfg::kQSmem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
   }
   const int bhc = p.B * p.H;
   kdkv<<<((p.M + 127) / 128) * bhc, Cfg::kThreads, Cfg::kKVSmem, s>>>(m.q64, m.do64, m.uq64, m.biasT, m.k128, m.v128,

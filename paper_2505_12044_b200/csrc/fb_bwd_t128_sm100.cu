@@ -570,12 +570,9 @@ template <int RP, bool BF16>
 static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, const BwdParams& p, cudaStream_t s) {
   using Cfg = T128Cfg<RP>;
   auto k = fb_bwd_t128_kernel<RP, BF16>;
-  static bool attr_done = false;  // host-side once per instantiation (benign race)
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_mask{0};
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(k), Cfg::kSmem);
+  if (e != cudaSuccess) return e;
   k<<<((p.M + 127) / 128) * p.B * p.H, 512, Cfg::kSmem, s>>>(m.q128, m.do128, m.uq128, m.k128, m.v128, m.uk128,
                                                             dqacc, p);
   return cudaGetLastError();

@@ -466,12 +466,9 @@ template <int D, int RP, bool DENSE, bool BF16>
 static cudaError_t launch_fwd_t(const FwdMaps& maps, const FwdParams& p, cudaStream_t stream) {
   using Cfg = FwdCfg<D, RP, DENSE, BF16>;
   auto kern = fb_fwd_kernel<D, RP, DENSE, BF16>;
-  static bool attr_done = false;  // set once per instantiation (host-side, benign race)
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_mask{0};
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(kern), Cfg::kSmemBytes);
+  if (e != cudaSuccess) return e;
   const int grid = p.num_pairs * p.B * p.H;
   kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(maps.q, maps.k, maps.v, maps.uq, maps.uk,
                                                           maps.bias, p);

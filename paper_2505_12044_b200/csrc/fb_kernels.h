@@ -5,9 +5,23 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <atomic>
 #include <type_traits>
 
 namespace fb {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the
+// attribute is per device, so a process driving several GPUs sets it on each.
+inline cudaError_t smem_attr_once(std::atomic<uint64_t>& mask, const void* kern, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 struct FwdParams {
   int B, H, N, M;

@@ -119,12 +119,9 @@ __global__ void __launch_bounds__(256) mlp_panels_kernel(MlpParams p) {
 
 cudaError_t launch_mlp_panels(const MlpParams& p, cudaStream_t s) {
   const size_t smem = (kTok * 8 + 2 * kTok * static_cast<size_t>(p.hidden) + kTok * static_cast<size_t>(p.R)) * 4;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_panels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_mask{0};
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(mlp_panels_kernel), 200 * 1024);
+  if (e != cudaSuccess) return e;
   mlp_panels_kernel<<<(p.L + kTok - 1) / kTok, 256, smem, s>>>(p);
   return cudaGetLastError();
 }

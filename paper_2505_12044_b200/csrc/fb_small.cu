@@ -651,13 +651,9 @@ template <int D>
 static cudaError_t launch_simt_tiled(const SimtParams& p, cudaStream_t s) {
   const int DK = D + p.R;
   const size_t smem = sizeof(float) * (static_cast<size_t>(DK) * 64 * 2 + 64 * D + 64 * 68);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fwd_simt_tiled_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_mask{0};
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(fwd_simt_tiled_kernel<D>), 200 * 1024);
+  if (e != cudaSuccess) return e;
   dim3 grid((p.N + 63) / 64, p.H, p.B);
   fwd_simt_tiled_kernel<D><<<grid, 256, smem, s>>>(p);
   return cudaGetLastError();
@@ -672,12 +668,9 @@ cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s) {
     return e;
   }
   const size_t smem = sizeof(float) * (kSimtRows * DK + kSimtKv * (DK | 1) + kSimtKv * p.D);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(fwd_simt_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_mask{0};
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(fwd_simt_f32_kernel), 200 * 1024);
+  if (e != cudaSuccess) return e;
   dim3 grid((p.N + kSimtRows - 1) / kSimtRows, p.H, p.B);
   fwd_simt_f32_kernel<<<grid, 128, smem, s>>>(p);
   note_launch();
