@@ -197,3 +197,31 @@ def test_bwd_t128_static_factors(B, H, N, M, R, causal, fb_):
         _bwd_case(B, H, N, M, 128, 0, causal, seed=3)
     else:
         _bwd_static_case(B, H, N, M, 128, R, causal, seed=B * 10 + R, factor_batch=fb_)
+
+
+@pytest.mark.parametrize("D,R,causal", [(128, 2, True), (128, 0, False), (64, 4, True)])
+def test_bwd_fp16_static(D, R, causal):
+    """fp16 inputs through the backward kernels (128x128-tile for d=128, fused 64-query for d=64)."""
+    B, H, N = 1, 2, 320
+    q, k, v = _qkv(B, H, N, N, D, torch.float16, seed=5)
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    do = torch.randn(B, H, N, D, device="cuda", generator=g).half()
+    mask = "causal" if causal else "none"
+    if R:
+        fq = torch.randn(1, H, N, R, device="cuda", generator=g) * 0.5
+        fk = torch.randn(1, H, N, R, device="cuda", generator=g) * 0.5
+        out = fb.flashbias_attention(q, k, v, fq, fk, mask=mask)
+    else:
+        fq = fk = None
+        out = fb.tiled_attention(q, k, v, mask=mask)
+    assert out.dtype == torch.float16
+    out.backward(do)
+    ref_leaves = [t.detach().double().requires_grad_(True) for t in (q, k, v)]
+    ref = ref_attention(*ref_leaves, None if fq is None else fq.double(), None if fk is None else fk.double(),
+                        causal=causal)
+    ref.backward(do.double())
+    for name, got, r_ in zip(["dq", "dk", "dv"], (q.grad, k.grad, v.grad), ref_leaves):
+        e = relerr(got, r_.grad)
+        assert e < BF16_TOL, f"{name}: rel err {e:.3e}"
