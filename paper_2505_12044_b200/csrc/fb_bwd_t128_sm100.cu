@@ -582,10 +582,10 @@ static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, con
 // shared memory; float4 loads along queries, 16-byte bf16 stores along the head dim.
 template <bool BF16>
 __global__ void __launch_bounds__(256) dq_convert_t_kernel(const float* __restrict__ acc, void* dq, int H, int N,
-                                                           int n4, int64_t sb, int64_t sh, int64_t sn) {
+                                                           int n4, int64_t sb, int64_t sh, int64_t sn, int plane0) {
   typedef typename std::conditional<BF16, __nv_bfloat16, __half>::type elem_t;
   __shared__ float tile[64][129];  // [query][dim], odd stride
-  const int bh = blockIdx.y, q0 = blockIdx.x * 64;
+  const int bh = plane0 + blockIdx.y, q0 = blockIdx.x * 64;
   const int bb = bh / H, hh = bh % H;
   const float* src = acc + static_cast<int64_t>(bh) * 128 * n4;
   const int t = threadIdx.x;
@@ -613,11 +613,14 @@ __global__ void __launch_bounds__(256) dq_convert_t_kernel(const float* __restri
 }
 
 cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, bool bf16, cudaStream_t s) {
-  dim3 grid((p.N + 63) / 64, p.B * p.H);
-  if (bf16)
-    dq_convert_t_kernel<true><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn);
-  else
-    dq_convert_t_kernel<false><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn);
+  const int planes = p.B * p.H;
+  for (int plane0 = 0; plane0 < planes; plane0 += 65535) {  // grid.y limit
+    dim3 grid((p.N + 63) / 64, planes - plane0 < 65535 ? planes - plane0 : 65535);
+    if (bf16)
+      dq_convert_t_kernel<true><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn, plane0);
+    else
+      dq_convert_t_kernel<false><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn, plane0);
+  }
   return cudaGetLastError();
 }
 
