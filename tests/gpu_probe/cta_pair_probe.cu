@@ -22,7 +22,7 @@ __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int MODE>
+template <int MODE, int MM = 256>
 __global__ void __launch_bounds__(128, 1) k(float* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(128, 1) k(float* out) {
   if (rank == 0 && t == 0) {
     const uint64_t ad = make_sdesc(smem_u32(A), 16, 256, 6);
     const uint64_t bd = make_sdesc(smem_u32(Bm), 16, 256, 6);
-    const uint32_t idesc = make_idesc(256, 128, false, false, true);
+    const uint32_t idesc = make_idesc(MM, 128, false, false, true);
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                  "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
                  "l"(ad), "l"(bd), "r"(idesc), "r"(0u) : "memory");
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(128, 1) k(float* out) {
   }
 }
 
-template <int MODE>
+template <int MODE, int MM = 256>
 void run(const char* nm) {
   float* d;
   cudaMalloc(&d, 2 * 128 * 128 * 4);
@@ -101,12 +101,22 @@ void run(const char* nm) {
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
   cfg.attrs = at; cfg.numAttrs = 1;
-  cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k<MODE>, d);
+  cudaFuncSetAttribute(k<MODE, MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k<MODE, MM>, d);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("%s: %s\n", nm, cudaGetErrorString(e)); cudaFree(d); return; }
   static float h[2 * 128 * 128];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  if (MM == 128) {  // report which (cta, lane) holds which A row: value / (n+1) at column 0
+    printf("%s: M=128 pair MMA, value at column 0 (= A row id) per cta/lane:\n", nm);
+    for (int r = 0; r < 2; ++r) {
+      printf("  cta %d lanes 0..127 (every 16th):", r);
+      for (int i = 0; i < 128; i += 16) printf(" %g", h[(r * 128 + i) * 128]);
+      printf("\n");
+    }
+    cudaFree(d);
+    return;
+  }
   int bad = 0;
   for (int r = 0; r < 2; ++r)
     for (int i = 0; i < 128; ++i)
@@ -127,5 +137,6 @@ void run(const char* nm) {
 int main() {
   run<0>("alloc cta_group::2");
   run<1>("alloc cta_group::1");
+  run<0, 128>("alloc cta_group::2");
   return 0;
 }
