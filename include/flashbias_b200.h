@@ -112,6 +112,10 @@ size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k);
  *           padded. */
 int fb_prepare_factors(const fb_tensor* f, int side, int split, float premul,
                        fb_tensor* out, void* stream);
+/* Both panels of a factor pair in one launch (uq = split(premul * fq), uk = split(fk));
+ * same layout contract as two fb_prepare_factors calls. */
+int fb_prepare_factor_pair(const fb_tensor* fq, const fb_tensor* fk, int split, float premul,
+                           fb_tensor* uq, fb_tensor* uk, void* stream);
 int64_t fb_factor_rpad(int64_t rank, int split);
 int64_t fb_factor_cols(int64_t rank, int split);
 

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "fb_attn_fwd", "fb_attn_bwd", "fb_bwd_workspace_bytes", "fb_prepare_factors",
     "fb_factor_rpad", "fb_factor_cols", "fb_fold_factor_grads", "fb_factor_alibi",
     "fb_factor_spatial", "fb_dense_from_factors", "fb_bwd_preprocess", "fb_last_error",
-    "fb_abi_version", "fb_launch_count", "fb_mlp_factor_panels",
+    "fb_abi_version", "fb_launch_count", "fb_mlp_factor_panels", "fb_prepare_factor_pair",
 )
 
 
@@ -68,6 +68,7 @@ def _declare(lib: ctypes.CDLL) -> None:
         "fb_abi_version": (i32, []),
         "fb_launch_count": (i64, [i32]),
         "fb_mlp_factor_panels": (i32, [_P, _P, _P, _P, _P, _P, _P, i32, i32, f32, _P, _P, vp]),
+        "fb_prepare_factor_pair": (i32, [_P, _P, i32, f32, _P, _P, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -204,8 +204,8 @@ def prepare_factor_panels(fq, fk, premul: float, split: int, dtype):
     uq = torch.empty(*fq32.shape[:-1], rpad, dtype=dtype, device=fq32.device)
     uk = torch.empty(*fk32.shape[:-1], rpad, dtype=dtype, device=fk32.device)
     s = _lib.stream_ptr(fq32.device)
-    _lib.check(lib.fb_prepare_factors(_lib.ref(_lib.desc(fq32)), 0, split, float(premul), _lib.ref(_lib.desc(uq)), s))
-    _lib.check(lib.fb_prepare_factors(_lib.ref(_lib.desc(fk32)), 1, split, 1.0, _lib.ref(_lib.desc(uk)), s))
+    D, ref = _lib.desc, _lib.ref
+    _lib.check(lib.fb_prepare_factor_pair(ref(D(fq32)), ref(D(fk32)), split, float(premul), ref(D(uq)), ref(D(uk)), s))
     return uq, uk
 
 

@@ -491,6 +491,24 @@ int fb_prepare_factors(const fb_tensor* f, int side, int split, float premul, fb
   return e == cudaSuccess ? FB_OK : cuda_fail(e, "prepare_factors");
 }
 
+int fb_prepare_factor_pair(const fb_tensor* fq, const fb_tensor* fk, int split, float premul, fb_tensor* uq,
+                           fb_tensor* uk, void* stream) {
+  if (!fq || !fk || !uq || !uk) return fail(FB_EVALUE, "null tensor");
+  if (split < 1 || split > 3) return fail(FB_EVALUE, "split must be 1, 2 or 3");
+  if (uq->dtype != FB_BF16 && uq->dtype != FB_F16) return fail(FB_EVALUE, "panels are bf16/f16");
+  if (fq->shape[3] < 1 || fq->shape[3] != fk->shape[3]) return fail(FB_ESHAPE, "factor ranks differ or are < 1");
+  for (int side = 0; side < 2; ++side) {
+    const fb_tensor* f = side ? fk : fq;
+    const fb_tensor* o = side ? uk : uq;
+    if (o->shape[3] < fb_factor_cols(f->shape[3], split)) return fail(FB_ESHAPE, "panel too narrow");
+    if (o->shape[2] != f->shape[2]) return fail(FB_ESHAPE, "panel rows differ from factor rows");
+    if (o->dtype != uq->dtype) return fail(FB_EVALUE, "uq and uk dtypes differ");
+  }
+  cudaError_t e = launch_prepare_factor_pair(to_t4(fq), to_t4(fk), split, premul, to_t4(uq), to_t4(uk),
+                                             reinterpret_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FB_OK : cuda_fail(e, "prepare_factor_pair");
+}
+
 int fb_mlp_factor_panels(const fb_tensor* x, const fb_tensor* w1, const fb_tensor* b1, const fb_tensor* w2,
                          const fb_tensor* b2, const fb_tensor* w3, const fb_tensor* b3, int side, int split,
                          float premul, fb_tensor* out, fb_tensor* factors, void* stream) {

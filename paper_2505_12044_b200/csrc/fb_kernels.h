@@ -116,6 +116,8 @@ struct Tensor4 {
 };
 cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul,
                                    const Tensor4& out, cudaStream_t s);
+cudaError_t launch_prepare_factor_pair(const Tensor4& fq, const Tensor4& fk, int split, float premul,
+                                       const Tensor4& uq, const Tensor4& uk, cudaStream_t s);
 cudaError_t launch_fold_factor_grads(const Tensor4& dpanel, int side, int split, float postmul,
                                      const Tensor4& out, cudaStream_t s);
 cudaError_t launch_factor_alibi(const float* slopes, int64_t heads, int64_t n, int64_t m,

@@ -86,13 +86,12 @@ __global__ void prepare_factors_kernel(Tensor4 f, int side, int split, float pre
 
 // Fast path: one thread per 8-column chunk of a panel row, one 16-byte store.
 template <bool BF16>
-__global__ void __launch_bounds__(256) prepare_factors_rows_kernel(Tensor4 f, int side, int split, float premul,
-                                                                   Tensor4 out) {
+__device__ __forceinline__ void prepare_rows_plane(const Tensor4& f, int side, int split, float premul,
+                                                   const Tensor4& out, int plane) {
   const int R = static_cast<int>(f.shape[3]);
   const int np = (split * (split + 1)) / 2;
   const int L = static_cast<int>(out.shape[2]), Hh = static_cast<int>(out.shape[1]);
   const int nch = static_cast<int>(out.shape[3]) / 8;
-  const int plane = blockIdx.y;
   const int64_t b = plane / Hh, h = plane % Hh;
   const float mul = side == 0 ? premul : 1.0f;
   const int odt = BF16 ? 1 : 2;
@@ -120,16 +119,60 @@ __global__ void __launch_bounds__(256) prepare_factors_rows_kernel(Tensor4 f, in
   }
 }
 
+template <bool BF16>
+__global__ void __launch_bounds__(256) prepare_factors_rows_kernel(Tensor4 f, int side, int split, float premul,
+                                                                   Tensor4 out) {
+  prepare_rows_plane<BF16>(f, side, split, premul, out, blockIdx.y);
+}
+
+// both panels in one launch: blockIdx.z = side (0: uq from fq with premul, 1: uk from fk)
+template <bool BF16>
+__global__ void __launch_bounds__(256) prepare_factor_pair_kernel(Tensor4 fq, Tensor4 fk, int split, float premul,
+                                                                  Tensor4 uq, Tensor4 uk) {
+  const int side = blockIdx.z;
+  const Tensor4& f = side == 0 ? fq : fk;
+  const Tensor4& out = side == 0 ? uq : uk;
+  if (blockIdx.y >= out.shape[0] * out.shape[1]) return;
+  prepare_rows_plane<BF16>(f, side, split, premul, out, blockIdx.y);
+}
+
+cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul, const Tensor4& out,
+                                   cudaStream_t s);
+
+static bool rows_ok(const Tensor4& out) {
+  return (out.dtype == 1 || out.dtype == 2) && out.stride[3] == 1 && out.shape[3] % 8 == 0 &&
+         out.stride[2] % 8 == 0 && out.stride[1] % 8 == 0 && out.stride[0] % 8 == 0 &&
+         (reinterpret_cast<uintptr_t>(out.data) % 16) == 0;
+}
+
+cudaError_t launch_prepare_factor_pair(const Tensor4& fq, const Tensor4& fk, int split, float premul,
+                                       const Tensor4& uq, const Tensor4& uk, cudaStream_t s) {
+  if (!rows_ok(uq) || !rows_ok(uk) || uq.dtype != uk.dtype) {
+    cudaError_t e = launch_prepare_factors(fq, 0, split, premul, uq, s);
+    return e != cudaSuccess ? e : launch_prepare_factors(fk, 1, split, 1.0f, uk, s);
+  }
+  const int64_t pq = uq.shape[0] * uq.shape[1], pk = uk.shape[0] * uk.shape[1];
+  const int64_t planes = pq > pk ? pq : pk;
+  const int64_t rows = uq.shape[2] > uk.shape[2] ? uq.shape[2] : uk.shape[2];
+  if (planes <= 0 || rows <= 0) return cudaSuccess;
+  if (planes > 65535) return cudaErrorInvalidValue;
+  int64_t gx = (rows * (uq.shape[3] / 8) + 255) / 256;
+  const int64_t cap = (148 * 16 + planes - 1) / planes;
+  if (gx > cap) gx = cap < 1 ? 1 : cap;
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(planes), 2);
+  if (uq.dtype == 1) prepare_factor_pair_kernel<true><<<grid, 256, 0, s>>>(fq, fk, split, premul, uq, uk);
+  else prepare_factor_pair_kernel<false><<<grid, 256, 0, s>>>(fq, fk, split, premul, uq, uk);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul,
                                    const Tensor4& out, cudaStream_t s) {
   const int64_t per_plane = out.shape[2] * out.shape[3];
   const int64_t planes = out.shape[0] * out.shape[1];
   if (per_plane <= 0 || planes <= 0) return cudaSuccess;
   if (planes > 65535 || per_plane > (int64_t(1) << 30)) return cudaErrorInvalidValue;
-  const bool rows_ok = (out.dtype == 1 || out.dtype == 2) && out.stride[3] == 1 && out.shape[3] % 8 == 0 &&
-                       out.stride[2] % 8 == 0 && out.stride[1] % 8 == 0 && out.stride[0] % 8 == 0 &&
-                       (reinterpret_cast<uintptr_t>(out.data) % 16) == 0;
-  if (rows_ok) {
+  if (rows_ok(out)) {
     int64_t gx = (out.shape[2] * (out.shape[3] / 8) + 255) / 256;
     const int64_t cap = (148 * 16 + planes - 1) / planes;
     if (gx > cap) gx = cap < 1 ? 1 : cap;
