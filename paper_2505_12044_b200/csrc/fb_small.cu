@@ -542,9 +542,9 @@ __global__ void __launch_bounds__(128) fwd_simt_f32_kernel(const SimtParams p) {
 // columns CPT*tx.. of O.  Q^T / K^T tiles are stored channel-major in shared
 // memory so every channel step is two float4 loads feeding 16 FMAs; P goes
 // through shared memory to the P.V product.
-template <int D>
+template <int D, int BM>
 __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p) {
-  constexpr int BM = 64, BN = 64, CPT = D / 16;
+  constexpr int BN = 64, CPT = D / 16, RT = BM / 16;  // rows per thread
   extern __shared__ float sm[];
   const int DK = D + p.R;
   float* sQ = sm;                  // [DK][BM]
@@ -564,10 +564,10 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
     }
     sQ[c * BM + r] = v;
   }
-  double m_run[4];
-  float l_run[4], acc[4][CPT];
+  double m_run[RT];
+  float l_run[RT], acc[RT][CPT];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < RT; ++i) {
     m_run[i] = -INFINITY;
     l_run[i] = 0.f;
 #pragma unroll
@@ -590,38 +590,49 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
       sV[idx] = j < p.M ? p.v[b * p.v_sb + h * p.v_sh + static_cast<int64_t>(j) * p.v_sn + c] : 0.f;
     }
     __syncthreads();
-    float s[4][4];
+    float s[RT][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
       for (int k = 0; k < 4; ++k) s[i][k] = 0.f;
+    auto qrow = [&](int c, float (&av)[RT]) {
+      if constexpr (RT == 4) {
+        const float4 a = *reinterpret_cast<const float4*>(sQ + c * BM + RT * ty);
+        av[0] = a.x; av[1] = a.y; av[2] = a.z; av[3] = a.w;
+      } else {
+        const float2 a = *reinterpret_cast<const float2*>(sQ + c * BM + RT * ty);
+        av[0] = a.x; av[1] = a.y;
+      }
+    };
 #pragma unroll 8
     for (int c = 0; c < D; ++c) {
-      const float4 a = *reinterpret_cast<const float4*>(sQ + c * BM + 4 * ty);
+      float av[RT];
+      qrow(c, av);
       const float4 kk = *reinterpret_cast<const float4*>(sK + c * BN + 4 * tx);
-      const float av[4] = {a.x, a.y, a.z, a.w}, kv[4] = {kk.x, kk.y, kk.z, kk.w};
+      const float kv[4] = {kk.x, kk.y, kk.z, kk.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
         for (int k = 0; k < 4; ++k) s[i][k] = fmaf(av[i], kv[k], s[i][k]);
     }
-    double su[4][4];
+    double su[RT][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
       for (int k = 0; k < 4; ++k) su[i][k] = 0.0;
     for (int c = D; c < DK; ++c) {
-      const float4 a = *reinterpret_cast<const float4*>(sQ + c * BM + 4 * ty);
+      float av[RT];
+      qrow(c, av);
       const float4 kk = *reinterpret_cast<const float4*>(sK + c * BN + 4 * tx);
-      const double av[4] = {a.x, a.y, a.z, a.w}, kv[4] = {kk.x, kk.y, kk.z, kk.w};
+      const double kv[4] = {kk.x, kk.y, kk.z, kk.w};
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) su[i][k] = fma(av[i], kv[k], su[i][k]);
+        for (int k = 0; k < 4; ++k) su[i][k] = fma(static_cast<double>(av[i]), kv[k], su[i][k]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int row = q0 + 4 * ty + i;
+    for (int i = 0; i < RT; ++i) {
+      const int row = q0 + RT * ty + i;
       double sd[4];
       double mx = -INFINITY;
 #pragma unroll
@@ -651,14 +662,14 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
       l_run[i] = l_run[i] * alpha + ps;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) acc[i][c] *= alpha;
-      *reinterpret_cast<float4*>(sP + (4 * ty + i) * PST + 4 * tx) = make_float4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<float4*>(sP + (RT * ty + i) * PST + 4 * tx) = make_float4(pk[0], pk[1], pk[2], pk[3]);
     }
     __syncthreads();
 #pragma unroll 4
     for (int j = 0; j < BN; ++j) {
-      float pv[4];
+      float pv[RT];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) pv[i] = sP[(4 * ty + i) * PST + j];
+      for (int i = 0; i < RT; ++i) pv[i] = sP[(RT * ty + i) * PST + j];
       float vv[CPT];
       if constexpr (CPT >= 4) {
 #pragma unroll
@@ -671,14 +682,14 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
         vv[0] = w.x; vv[1] = w.y;
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
         for (int c = 0; c < CPT; ++c) acc[i][c] = fmaf(pv[i], vv[c], acc[i][c]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = q0 + 4 * ty + i;
+  for (int i = 0; i < RT; ++i) {
+    const int row = q0 + RT * ty + i;
     if (row >= p.N) continue;
     const float inv = l_run[i] > 0.f ? 1.0f / l_run[i] : 0.f;
 #pragma unroll
@@ -690,16 +701,23 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
   }
 }
 
+template <int D, int BM>
+static cudaError_t launch_simt_tiled_bm(const SimtParams& p, cudaStream_t s) {
+  const int DK = D + p.R;
+  const size_t smem = sizeof(float) * (static_cast<size_t>(DK) * (BM + 64) + 64 * D + BM * 68);
+  static std::atomic<uint64_t> attr_mask{0};
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(fwd_simt_tiled_kernel<D, BM>), 200 * 1024);
+  if (e != cudaSuccess) return e;
+  dim3 grid((p.N + BM - 1) / BM, p.H, p.B);
+  fwd_simt_tiled_kernel<D, BM><<<grid, 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
 template <int D>
 static cudaError_t launch_simt_tiled(const SimtParams& p, cudaStream_t s) {
-  const int DK = D + p.R;
-  const size_t smem = sizeof(float) * (static_cast<size_t>(DK) * 64 * 2 + 64 * D + 64 * 68);
-  static std::atomic<uint64_t> attr_mask{0};
-  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(fwd_simt_tiled_kernel<D>), 200 * 1024);
-  if (e != cudaSuccess) return e;
-  dim3 grid((p.N + 63) / 64, p.H, p.B);
-  fwd_simt_tiled_kernel<D><<<grid, 256, smem, s>>>(p);
-  return cudaGetLastError();
+  // 32-row CTAs when 64-row ones would not fill two waves of the 148 SMs
+  const int64_t ctas64 = static_cast<int64_t>((p.N + 63) / 64) * p.H * p.B;
+  return ctas64 < 2 * 148 ? launch_simt_tiled_bm<D, 32>(p, s) : launch_simt_tiled_bm<D, 64>(p, s);
 }
 
 cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s) {
