@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128, 1) k(float* out) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (t == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
   if (warp == 0) {
-    if (MODE == 0) {
+    if (MODE != 1) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tbase)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
@@ -61,7 +61,31 @@ __global__ void __launch_bounds__(128, 1) k(float* out) {
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = tbase;
-  if (rank == 0 && t == 0) {
+  if (MODE == 2) {  // stage A (this CTA's 128 rows x 16 bf16 = 8 packed columns) into TMEM columns [128, 136)
+    uint32_t pk[8];
+    for (int c = 0; c < 8; ++c) {
+      const float lo = c == 0 ? static_cast<float>(128 * rank + t) : 0.f;
+      __nv_bfloat162 v2 = __floats2bfloat162_rn(lo, 0.f);
+      pk[c] = *reinterpret_cast<uint32_t*>(&v2);
+    }
+    const uint32_t lane_off0 = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tmem + lane_off0 + 128),
+                 "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3]), "r"(pk[4]), "r"(pk[5]), "r"(pk[6]), "r"(pk[7]) : "memory");
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+  }
+  if (rank == 0 && t == 0 && MODE == 2) {
+    const uint64_t bd = make_sdesc(smem_u32(Bm), 16, 256, 6);
+    const uint32_t idesc = make_idesc(MM, 128, false, false, true);
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem),
+                 "r"(tmem + 128), "l"(bd), "r"(idesc), "r"(0u) : "memory");
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(&bar)), "h"((uint16_t)3) : "memory");
+  } else if (rank == 0 && t == 0) {
     const uint64_t ad = make_sdesc(smem_u32(A), 16, 256, 6);
     const uint64_t bd = make_sdesc(smem_u32(Bm), 16, 256, 6);
     const uint32_t idesc = make_idesc(MM, 128, false, false, true);
@@ -85,7 +109,7 @@ __global__ void __launch_bounds__(128, 1) k(float* out) {
   cluster_sync();
   if (warp == 0) {
     tc_fence_after();
-    if (MODE == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (MODE != 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem));
     else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
   }
 }
@@ -138,5 +162,6 @@ int main() {
   run<0>("alloc cta_group::2");
   run<1>("alloc cta_group::1");
   run<0, 128>("alloc cta_group::2");
+  run<2>("TS pair MMA (A from TMEM)");
   return 0;
 }
