@@ -23,7 +23,6 @@ namespace fb {
 
 static thread_local char g_err[512] = "";
 static thread_local int64_t g_launches = 0;
-static int g_force_split_bwd = 0;  // testing hook: FB_FORCE_SPLIT_BWD=1 selects the two-kernel backward
 
 void note_launch(int n) { g_launches += n; }
 
@@ -405,8 +404,8 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     const char* v = getenv("FB_FORCE_SPLIT_BWD");
     return v && v[0] == '1' ? 1 : 0;
   }();
-  g_force_split_bwd = force_split;
-  const bool fused = !g_force_split_bwd && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
+  // testing hook: FB_FORCE_SPLIT_BWD=1 selects the deterministic two-kernel backward (read once, immutable)
+  const bool fused = !force_split && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
   if (fused) {
     float* acc = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(delta) +
                                           ((size_t)B * H * N * sizeof(float) + 255) / 256 * 256);
