@@ -69,6 +69,40 @@ def alibi_slopes(h: int):
     return [-(2.0 ** (-8.0 * (i + 1) / h)) for i in range(h)]
 
 
+def c5_bias(n: int, seed: int, device, rank: int = 64):
+    """SURVEY §8(d) C5 per-(b,h) dense bias, generated on device (fp32):
+    b = sum_{k<=rank} 8 * 0.9^(k-1) u_k v_k^T + 1e-3 E, u_k, v_k unit random
+    vectors, E ~ N(0, 1); seed = 5000 + b*H + h."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(seed)
+    u = torch.randn(n, rank, generator=g, device=device)
+    v = torch.randn(n, rank, generator=g, device=device)
+    u = u / u.norm(dim=0, keepdim=True)
+    v = v / v.norm(dim=0, keepdim=True)
+    w = 8.0 * 0.9 ** torch.arange(rank, device=device, dtype=torch.float32)
+    return (u * w) @ v.T + 1e-3 * torch.randn(n, n, generator=g, device=device)
+
+
+def af3_pair_bias(n: int, heads, device):
+    """SURVEY §8(d) C4 AlphaFold3-style pair bias [len(heads), n, n] (fp64 on device):
+    residue coordinates from a 3.8 A random walk (Rng(4000)), 16 RBF channels
+    z_ijk = exp(-(|x_i - x_j| - mu_k)^2 / (2 * 2.5^2)), mu_k = 2 + 2.5k, and
+    per-head weights w_h ~ N(0, 1/16) (Rng(4100 + h)): b_h = z . w_h."""
+    import numpy as np
+    import torch
+
+    from paper_2505_12044_b200.rng import Rng
+    steps = Rng(4000).normal(n, 3)
+    steps = 3.8 * steps / np.linalg.norm(steps, axis=1, keepdims=True)
+    x = torch.as_tensor(np.cumsum(steps, axis=0), device=device, dtype=torch.float64)
+    dist = torch.cdist(x, x)
+    mu = 2.0 + 2.5 * torch.arange(16, device=device, dtype=torch.float64)
+    z = torch.exp(-((dist[..., None] - mu) ** 2) / (2 * 2.5 ** 2))  # [n, n, 16]
+    w = torch.stack([torch.as_tensor(Rng(4100 + h).normal(16), device=device, dtype=torch.float64) / 4.0
+                     for h in heads])  # [H, 16], std 1/4
+    return torch.einsum("ijk,hk->hij", z, w)
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -262,10 +296,14 @@ def kernel_breakdown(cfg, inp, reps: int = 3):
     mask_code = 1 if cfg["causal"] else 0
     d = cfg["d"]
     q, k, v, do = (t.detach() for t in (inp["q"], inp["k"], inp["v"], inp["do"]))
-    premul = math.sqrt(d)
-    split = A.choose_split_cached(inp["fq"], inp["fk"], premul, max_cols=64 if d == 128 else 128)  # as the step
-    uq, uk = A.prepare_factor_panels(inp["fq"].detach(), inp["fk"].detach(), premul, split, q.dtype)
     scale = 1.0 / math.sqrt(d)
+    plan = A.plan_factor_fold_cached(inp["fq"], inp["fk"], inp["fq"], inp["fk"], scale,
+                                     max_cols=64 if d == 128 else 128)  # as the step
+    split = plan.split
+    uq, uk = A.prepare_factor_panels(inp["fq"].detach(), inp["fk"].detach(), plan.premul, split, q.dtype)
+    if plan.q_fold:
+        q = (q * scale).contiguous()
+    scale = plan.kernel_scale
     out = {}
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     o = lse = None
@@ -283,6 +321,7 @@ def kernel_breakdown(cfg, inp, reps: int = 3):
     out["fwd_ms"] = statistics.median(fwd_ms[1:])
     out["bwd_ms"] = statistics.median(bwd_ms[1:]) if cfg["bwd"] else 0.0
     out["split"] = split
+    out["q_fold"] = plan.q_fold
     out["rpad"] = int(uq.shape[-1])
     del _lib
     return out
@@ -398,7 +437,7 @@ def run_gpu(args, cfg):
             "fwd_ms": round(kb["fwd_ms"], 3), "bwd_ms": round(kb["bwd_ms"], 3),
             "fwd_tflops": round(fwd_flops_loc / (kb["fwd_ms"] * 1e-3) / 1e12, 1),
             "bwd_tflops": round(bwd_flops_loc / (kb["bwd_ms"] * 1e-3) / 1e12, 1) if cfg["bwd"] else None,
-            "factor_split": kb["split"], "factor_rpad": kb["rpad"],
+            "factor_split": kb["split"], "factor_rpad": kb["rpad"], "q_fold": kb["q_fold"],
         }
 
     e2e = run_e2e(cfg, inp, args, device, dist=dist, total_bh=total_bh) if not args.skip_e2e else None

@@ -22,7 +22,7 @@
  *   fb_factor_spatial  decompose_spatial        decompose.py:55-81
  *   fb_fold_factor_grads  chain rule from split columns back to logical
  *                      factors (inverse of fb_prepare_factors)
- *   fb_dense_bias      generate_bias (AlibiBias / SpatialDistanceBias)
+ *   fb_dense_from_factors  generate_bias (AlibiBias / SpatialDistanceBias)
  *                      bias.py:158-178 (dense-baseline input, K8)
  *
  * Error codes map onto the reference exception taxonomy (errors.py:4-25):
@@ -161,8 +161,9 @@ int fb_bwd_preprocess(const fb_tensor* o, const fb_tensor* dout,
 
 const char* fb_last_error(void);
 int fb_abi_version(void);
-/* Number of kernel launches issued by this library on the calling thread
- * since the last reset (instrumentation for bench.py "gpu_launches"). */
+/* Number of kernel launches issued by this library in this process (all
+ * threads, including autograd's backward thread) since the last reset
+ * (instrumentation for bench.py "gpu_launches"). */
 int64_t fb_launch_count(int reset);
 
 #ifdef __cplusplus

@@ -145,6 +145,51 @@ def attention_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, bias=None, mask="no
     return res
 
 
+def blocked_attention_fwd_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, mask="none", scale=None,
+                              block=1024):
+    """attention_bwd for ONE 2-D head at full config size, streamed over query
+    blocks so memory stays O(block * M) (a 16384^2 float64 logit matrix would
+    be 2 GiB per array).  Same arithmetic as attention_bwd (its analytic
+    gradient of ref attention.py:111-137 / 205-230), row block by row block:
+    each block sees all the keys it can attend to, so its softmax, O rows, dS
+    rows, dq rows and dfq rows are final and its dK, dV, dfk contributions are
+    summed.  Returns dict(o, lse, dq, dk, dv[, dfq, dfk])."""
+    q, k, v, do = (np.asarray(x, dtype=np.float64) for x in (q, k, v, do))
+    scale = 1.0 / math.sqrt(q.shape[-1]) if scale is None else scale
+    n, m = q.shape[0], k.shape[0]
+    if fq is not None:
+        fq = np.asarray(fq, np.float64) * premul
+        fk = np.asarray(fk, np.float64)
+    res = {"o": np.empty((n, v.shape[1])), "lse": np.empty(n), "dq": np.empty_like(q),
+           "dk": np.zeros_like(k), "dv": np.zeros_like(v)}
+    if fq is not None:
+        res["dfq"], res["dfk"] = np.empty_like(fq), np.zeros_like(fk)
+    for q0 in range(0, n, block):
+        q1 = min(q0 + block, n)
+        m1 = min(m, q1) if mask == "causal" else m  # keys any row of the block can see
+        s = (q[q0:q1] @ k[:m1].T) * scale
+        if fq is not None:
+            s += (fq[q0:q1] @ fk[:m1].T) * scale
+        if mask == "causal":
+            s[np.arange(m1)[None, :] > np.arange(q0, q1)[:, None]] = -np.inf
+        mx = s.max(axis=1, keepdims=True)
+        p = np.exp(s - mx)
+        den = p.sum(axis=1, keepdims=True)
+        p /= den
+        o = p @ v[:m1]
+        dp = do[q0:q1] @ v[:m1].T
+        ds = p * (dp - (do[q0:q1] * o).sum(axis=1, keepdims=True))
+        res["o"][q0:q1] = o
+        res["lse"][q0:q1] = (mx + np.log(den))[:, 0]
+        res["dq"][q0:q1] = scale * ds @ k[:m1]
+        res["dk"][:m1] += scale * ds.T @ q[q0:q1]
+        res["dv"][:m1] += p.T @ do[q0:q1]
+        if fq is not None:
+            res["dfq"][q0:q1] = scale * premul * ds @ fk[:m1]
+            res["dfk"][:m1] += scale * premul * ds.T @ (fq[q0:q1] / premul)
+    return res
+
+
 def _reduce_to(x, shape):
     """Sum x over dims where ``shape`` broadcasts (size 1 / missing)."""
     while x.ndim > len(shape):

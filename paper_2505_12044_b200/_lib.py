@@ -18,12 +18,6 @@ from .errors import ConfigError, MaskError, ShapeError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libflashbias_b200.so")
-# debug only: FLASHBIAS_B200_TRACE=1 loads the timeline-trace build instead
-if os.environ.get("FLASHBIAS_B200_TRACE") == "1":
-    LIB_PATH = os.path.join(_HERE, "_lib", "libflashbias_b200_trace.so")
-# debug only: FLASHBIAS_B200_VARIANT=name loads _lib/libflashbias_b200_<name>.so (tests/gpu_probe experiments)
-if os.environ.get("FLASHBIAS_B200_VARIANT"):
-    LIB_PATH = os.path.join(_HERE, "_lib", "libflashbias_b200_%s.so" % os.environ["FLASHBIAS_B200_VARIANT"])
 
 FB_F32, FB_BF16, FB_F16, FB_F64 = 0, 1, 2, 3
 MASK_CODES = {"none": 0, "causal": 1}

@@ -4,11 +4,13 @@ Public names and argument meaning follow the reference:
 
 * ``flashbias_attention(q, k, v, fq, fk, mask="none", tiles=None)``
   (attention.py:205-230): logits = q k^T / sqrt(C) + fq fk^T with C the
-  ORIGINAL channel count; computed as the widened contraction
-  [q | sqrt(C) fq][k | fk]^T / sqrt(C) inside the tcgen05 kernel (K1).
+  ORIGINAL channel count; computed as a widened contraction inside the
+  tcgen05 kernel (K1): [q | sqrt(C) fq][k | fk]^T / sqrt(C) (the reference
+  order) or Q' = [q / sqrt(C), fq], K' = [k, fk] (north_star fold, chosen when
+  it needs fewer bf16 split columns -- see FactorPlan).
 * ``tiled_attention(q, k, v, bias=NO_BIAS, mask, tiles, scale)``
   (attention.py:140-202): NoBias / DenseBias (K3, bias tile streamed by TMA) /
-  FactoredBias (K1 with premultiplier 1/scale so the factor term is unscaled).
+  FactoredBias (K1, the factor term unscaled).
 * ``reference_attention`` / ``attention_weights`` (attention.py:111-137): the
   materialised formula, evaluated on the GPU with torch (validation helper).
 * ``TileConfig`` / ``choose_tile_sizes`` (attention.py:38-74): kept for API
@@ -145,67 +147,166 @@ def _padded_head_dim(c: int) -> int:
 _SPLIT_CACHE: dict = {}
 
 
-def _split_key(fq, fk, premul, tol, max_cols):
-    """Identity of a factor pair for the split cache: storage, shape and the
-    in-place version counters (any write to the factors invalidates it)."""
-    def ident(t):
-        return (t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype, t._version)
-    return ident(fq), ident(fk), float(premul), float(tol), int(max_cols)
+@dataclass(frozen=True)
+class FactorPlan:
+    """How a factor pair enters the widened contraction (north_star fold).
+
+    The logits are ``s * q.k + fq.fk``.  ``q_fold`` False: the reference order
+    (attention.py:225-230), uq = split(fq / s) and the kernel scales the whole
+    product by s.  ``q_fold`` True: Q' = [s * q, U], K' = [k, V] -- the kernel
+    scale is 1, q is pre-scaled (one bf16 rounding of q) and uq = split(fq),
+    so bf16-exact SVD / neural factors need no split even when 1/s = sqrt(C)
+    is not a power of two.  ``split`` is the bf16 k-way split level."""
+
+    split: int
+    q_fold: bool
+    premul: float
+    kernel_scale: float
 
 
-def choose_split_cached(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int = 64) -> int:
-    """choose_split memoised per factor tensors (the decision needs a device->host
-    read; static factors such as ALiBi/spatial pay it once, not every call)."""
-    key = _split_key(fq, fk, premul, tol, max_cols)
-    k = _SPLIT_CACHE.get(key)
+def _is_pow2(x: float) -> bool:
+    return x > 0 and math.frexp(x)[0] == 0.5
+
+
+def _part_stats(x64, x32, pdt, dims):
+    """Per-rank magnitudes of the k-way split the prepare kernel builds from the
+    fp32 value x32 (fb_small.cu split_part: successive residual roundings to the
+    panel dtype): P[i] = max|part_i| (i < 3), Rs[k] = max|x_exact - sum_{i<k} part_i|
+    (k = 1..3; includes the fp32 rounding of premul*f), X = max|x_exact|."""
+    import torch
+    rem = x32.clone()
+    acc = torch.zeros_like(x64)
+    P, Rs = [], []
+    for _ in range(3):
+        part = rem.to(pdt).float()
+        rem = rem - part
+        acc = acc + part.double()
+        P.append(part.abs().amax(dim=dims))
+        Rs.append((x64 - acc).abs().amax(dim=dims))
+    return P, Rs, x64.abs().amax(dim=dims)
+
+
+def _split_bounds(fq, fk, premuls, pdt=None):
+    """One device->host read: for each premul, the worst-case |logit term error|
+    (in units of premul*fq.fk) of the k-way split for k = 1, 2, 3:
+      sum_r [ sum_{i,j<k, i+j>=k} P_a[i] P_b[j] + Ra[k] max|b| + (max|a| + Ra[k]) Rb[k] ]
+    (a = premul*fq, b = fk; the kept columns are the part pairs i + j <= k-1)."""
+    import torch
+    pdt = pdt or torch.bfloat16
+    dims_a = tuple(range(fq.dim() - 1))
+    dims_b = tuple(range(fk.dim() - 1))
+    b64 = fk.detach().double()
+    Pb, Rb, Xb = _part_stats(b64, fk.detach().float(), pdt, dims_b)
+    rows = []
+    for pm in premuls:
+        a64 = fq.detach().double() * pm
+        Pa, Ra, Xa = _part_stats(a64, fq.detach().float() * pm, pdt, dims_a)
+        for k in (1, 2, 3):
+            t = Ra[k - 1] * Xb + (Xa + Ra[k - 1]) * Rb[k - 1]
+            for i in range(k):
+                for j in range(k):
+                    if i + j >= k:
+                        t = t + Pa[i] * Pb[j]
+            rows.append(t.sum())
+    vals = torch.stack(rows).cpu().tolist()
+    return [vals[3 * n: 3 * n + 3] for n in range(len(premuls))]
+
+
+def _split_level(bounds, logit_scale: float, r: int, tol: float, max_cols: int) -> Optional[int]:
+    """Smallest k in {1,2,3} with logit_scale * bound_k <= tol and R k(k+1)/2 <= max_cols; None if none."""
+    for k in (1, 2, 3):
+        if r * k * (k + 1) // 2 > max_cols:
+            return None
+        b = bounds[k - 1] * logit_scale
+        if b == b and b <= tol:  # NaN/inf (e.g. fp16 overflow) never qualifies
+            return k
+    return None
+
+
+def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int = 64, logit_scale=None,
+                 panel_dtype=None) -> int:
+    """bf16 k-way split level for logical fp32 factors (SURVEY §7.3 H1).
+
+    The smallest k whose worst-case error on the logit term, logit_scale *
+    |premul fq.fk - sum of the kept part products| (default logit_scale =
+    1/premul: the reference fold, logits = (1/premul) * (premul fq).fk), is
+    within ``tol`` with R * k(k+1)/2 <= max_cols columns.  Raises ConfigError
+    when no level meets the bound inside the panel budget (it never silently
+    drops below it)."""
+    ls = 1.0 / premul if logit_scale is None else logit_scale
+    bounds = _split_bounds(fq, fk, [premul], panel_dtype)[0]
+    k = _split_level(bounds, ls, int(fq.shape[-1]), tol, max_cols)
     if k is None:
-        if len(_SPLIT_CACHE) > 256:
-            _SPLIT_CACHE.clear()
-        k = _SPLIT_CACHE[key] = choose_split(fq, fk, premul, tol, max_cols)
+        raise ConfigError(
+            f"rank-{fq.shape[-1]} factors need more than {max_cols} panel columns to stay within {tol:g} logits "
+            f"(k=1..3 error bounds {[round(b * ls, 6) for b in bounds]}); pass bf16-exact factors, a lower rank, "
+            f"or use the fp32 path")
     return k
 
 
-def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int = 64) -> int:
-    """bf16 k-way split level for logical fp32 factors (SURVEY §7.3 H1).
+def plan_factor_fold(fq, fk, scale: float, tol: float = 1e-2, max_cols: int = 64, panel_dtype=None) -> FactorPlan:
+    """Pick the fold and split for logits = scale*q.k + fq.fk (see FactorPlan).
 
-    1 when both factors are exactly representable in bf16; otherwise the
-    smallest k whose error bound sum_r |a_r|max |b_r|max * k * 2^(-8k-1) is
-    below ``tol`` (logit units), limited by R * k(k+1)/2 <= max_cols.
-    """
-    import torch
-    a = fq.detach().float() * premul
-    b = fk.detach().float()
-    r = a.shape[-1]
-    amax = a.abs().amax(dim=tuple(range(a.dim() - 1)))
-    bmax = b.abs().amax(dim=tuple(range(b.dim() - 1)))
-    inexact = ((a.to(torch.bfloat16).float() != a).any() | (b.to(torch.bfloat16).float() != b).any()).float()
-    stats = torch.stack([inexact, (amax * bmax).sum()]).cpu()  # one device->host read
-    if stats[0] == 0:
-        return 1
-    scale = float(stats[1])
-    best = 1
-    for k in (1, 2, 3):
-        if r * k * (k + 1) // 2 > max_cols:
-            break
-        best = k
-        if scale * k * 2.0 ** (-8 * k - 1) <= tol:
-            return k
-    return best
+    The reference order is kept whenever 1/scale is a power of two (exact) or
+    it needs no more columns; otherwise Q' = [scale*q, U] avoids the
+    premultiplier's rounding.  Raises ConfigError if neither meets ``tol``."""
+    pm = 1.0 / scale
+    r = int(fq.shape[-1])
+    if _is_pow2(pm):
+        ba = _split_bounds(fq, fk, [pm], panel_dtype)[0]
+        ka, kq, bq = _split_level(ba, scale, r, tol, max_cols), None, None
+    else:
+        ba, bq = _split_bounds(fq, fk, [pm, 1.0], panel_dtype)
+        ka = _split_level(ba, scale, r, tol, max_cols)
+        kq = _split_level(bq, 1.0, r, tol, max_cols)
+    if ka is not None and (kq is None or ka <= kq):
+        return FactorPlan(ka, False, pm, scale)
+    if kq is not None:
+        return FactorPlan(kq, True, 1.0, 1.0)
+    raise ConfigError(
+        f"rank-{r} factors need more than {max_cols} panel columns to stay within {tol:g} logits "
+        f"(k=1..3 error bounds {[round(b * scale, 6) for b in ba]}); pass bf16-exact factors, a lower rank, "
+        f"or use the fp32 path")
+
+
+def plan_factor_fold_cached(fq_user, fk_user, fq, fk, scale: float, tol: float = 1e-2,
+                            max_cols: int = 64, panel_dtype=None) -> FactorPlan:
+    """plan_factor_fold memoised per user factor OBJECTS (the decision needs a
+    device->host read; static factors such as ALiBi/spatial pay it once).  The
+    entry is reused only while weak references still resolve to the very same
+    tensors at the same in-place version, so a new tensor that happens to reuse
+    a freed allocation never inherits a stale split level.  numpy inputs (a
+    fresh device copy every call) are not cached."""
+    import weakref
+    if not (_is_torch(fq_user) and _is_torch(fk_user)):
+        return plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype)
+    key = (id(fq_user), id(fk_user), fq_user._version, fk_user._version, float(scale), float(tol), int(max_cols),
+           str(panel_dtype))
+    hit = _SPLIT_CACHE.get(key)
+    if hit is not None and hit[0]() is fq_user and hit[1]() is fk_user:
+        return hit[2]
+    plan = plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype)
+    if len(_SPLIT_CACHE) > 256:
+        _SPLIT_CACHE.clear()
+    _SPLIT_CACHE[key] = (weakref.ref(fq_user), weakref.ref(fk_user), plan)
+    return plan
 
 
 def prepare_factor_panels(fq, fk, premul: float, split: int, dtype):
     """Device-ready panels (fb_prepare_factors): uq = split(premul*fq), uk = split(fk)."""
     import torch
     lib = _lib.lib()
-    fq32 = fq.float().contiguous()
-    fk32 = fk.float().contiguous()
-    r = fq32.shape[-1]
-    rpad = int(lib.fb_factor_rpad(r, split))
-    uq = torch.empty(*fq32.shape[:-1], rpad, dtype=dtype, device=fq32.device)
-    uk = torch.empty(*fk32.shape[:-1], rpad, dtype=dtype, device=fk32.device)
-    s = _lib.stream_ptr(fq32.device)
-    D, ref = _lib.desc, _lib.ref
-    _lib.check(lib.fb_prepare_factor_pair(ref(D(fq32)), ref(D(fk32)), split, float(premul), ref(D(uq)), ref(D(uk)), s))
+    with torch.cuda.device(fq.device):
+        fq32 = fq.float().contiguous()
+        fk32 = fk.float().contiguous()
+        r = fq32.shape[-1]
+        rpad = int(lib.fb_factor_rpad(r, split))
+        uq = torch.empty(*fq32.shape[:-1], rpad, dtype=dtype, device=fq32.device)
+        uk = torch.empty(*fk32.shape[:-1], rpad, dtype=dtype, device=fk32.device)
+        s = _lib.stream_ptr(fq32.device)
+        D, ref = _lib.desc, _lib.ref
+        _lib.check(lib.fb_prepare_factor_pair(ref(D(fq32)), ref(D(fk32)), split, float(premul), ref(D(uq)),
+                                              ref(D(uk)), s))
     return uq, uk
 
 
@@ -213,9 +314,10 @@ def fold_factor_grads(dpanel, like, side: int, split: int, postmul: float):
     """fb_fold_factor_grads: split-panel gradients -> logical factor gradient shaped like ``like``."""
     import torch
     lib = _lib.lib()
-    out = torch.empty(like.shape, dtype=torch.float32, device=dpanel.device)
-    _lib.check(lib.fb_fold_factor_grads(_lib.ref(_lib.desc(dpanel)), side, split, float(postmul),
-                                        _lib.ref(_lib.desc(out)), _lib.stream_ptr(dpanel.device)))
+    with torch.cuda.device(dpanel.device):
+        out = torch.empty(like.shape, dtype=torch.float32, device=dpanel.device)
+        _lib.check(lib.fb_fold_factor_grads(_lib.ref(_lib.desc(dpanel)), side, split, float(postmul),
+                                            _lib.ref(_lib.desc(out)), _lib.stream_ptr(dpanel.device)))
     return out
 
 
@@ -224,12 +326,13 @@ def _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale, need_lse=True):
     import torch
     lib = _lib.lib()
     B, H, N, _ = q.shape
-    o = torch.empty(B, H, N, v.shape[-1], dtype=q.dtype, device=q.device)
-    lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device) if need_lse else None
-    D = _lib.desc
-    _lib.check(lib.fb_attn_fwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
-                               _lib.ref(D(bias)), mask_code, float(scale), _lib.ref(D(o)), _lib.ref(D(lse)),
-                               _lib.stream_ptr(q.device)))
+    with torch.cuda.device(q.device):
+        o = torch.empty(B, H, N, v.shape[-1], dtype=q.dtype, device=q.device)
+        lse = torch.empty(B, H, N, dtype=torch.float32, device=q.device) if need_lse else None
+        D = _lib.desc
+        _lib.check(lib.fb_attn_fwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
+                                   _lib.ref(D(bias)), mask_code, float(scale), _lib.ref(D(o)), _lib.ref(D(lse)),
+                                   _lib.stream_ptr(q.device)))
     return o, lse
 
 
@@ -237,21 +340,23 @@ def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad)
     import torch
     lib = _lib.lib()
     D = _lib.desc
-    dq = torch.empty_like(q)
-    dk = torch.empty_like(k)
-    dv = torch.empty_like(v)
-    duq = duk = None
-    if want_fgrad and uq is not None:
-        B, H = q.shape[0], q.shape[1]
-        duq = torch.empty(B, H, q.shape[2], uq.shape[-1], dtype=torch.float32, device=q.device)
-        duk = torch.empty(B, H, k.shape[2], uk.shape[-1], dtype=torch.float32, device=q.device)
-    dq_d, k_d = D(q), D(k)
-    ws_bytes = int(lib.fb_bwd_workspace_bytes(_lib.ref(dq_d), _lib.ref(k_d)))
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
-    _lib.check(lib.fb_attn_bwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
-                               _lib.ref(D(bias)), _lib.ref(D(o)), _lib.ref(D(lse)), _lib.ref(D(do)), mask_code,
-                               float(scale), _lib.ref(D(dq)), _lib.ref(D(dk)), _lib.ref(D(dv)), _lib.ref(D(duq)),
-                               _lib.ref(D(duk)), ws.data_ptr(), ws_bytes, _lib.stream_ptr(q.device)))
+    with torch.cuda.device(q.device):
+        dq = torch.empty_like(q)
+        dk = torch.empty_like(k)
+        dv = torch.empty_like(v)
+        duq = duk = None
+        if want_fgrad and uq is not None:
+            B, H = q.shape[0], q.shape[1]
+            duq = torch.empty(B, H, q.shape[2], uq.shape[-1], dtype=torch.float32, device=q.device)
+            duk = torch.empty(B, H, k.shape[2], uk.shape[-1], dtype=torch.float32, device=q.device)
+        dq_d, k_d = D(q), D(k)
+        ws_bytes = int(lib.fb_bwd_workspace_bytes(_lib.ref(dq_d), _lib.ref(k_d)))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
+        _lib.check(lib.fb_attn_bwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
+                                   _lib.ref(D(bias)), _lib.ref(D(o)), _lib.ref(D(lse)), _lib.ref(D(do)), mask_code,
+                                   float(scale), _lib.ref(D(dq)), _lib.ref(D(dk)), _lib.ref(D(dv)),
+                                   _lib.ref(D(duq)), _lib.ref(D(duk)), ws.data_ptr(), ws_bytes,
+                                   _lib.stream_ptr(q.device)))
     return dq, dk, dv, duq, duk
 
 
@@ -282,6 +387,7 @@ def _make_fn():
                                                want_fg)
             dfq = dfk = None
             if want_fg:
+                # the kernel's duq is d/d(uq) of scale*uq.uk; uq = premul*fq -> dfq = premul*duq
                 dfq = fold_factor_grads(duq, fq, 0, split, premul).to(fq.dtype)
                 dfk = fold_factor_grads(duk, fk, 1, split, 1.0).to(fk.dtype)
             return dq, dk, dv, dfq, dfk, None, None, None, None, None
@@ -299,9 +405,13 @@ def _fn():
     return _FN
 
 
-def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none", scale=None,
-               precision=None, split=None):
-    """Shared driver: normalise inputs, run the kernel, mirror the input layout."""
+def _needs_grad(*ts) -> bool:
+    return any(t is not None and _is_torch(t) and t.requires_grad for t in ts)
+
+
+def _attention(q, k, v, *, fq=None, fk=None, bias=None, mask="none", scale=None, precision=None, split=None):
+    """Shared driver: logits = scale*q.k + fq.fk + bias (+ causal); normalise
+    inputs, run the kernel, mirror the input layout."""
     import torch
     shp = _Shape(q)
     _validate_qkv_shapes(q, k, v)
@@ -313,6 +423,12 @@ def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none",
         raise RuntimeError("flashbias: CUDA device required (no CPU fallback)")
     device = shp.device if (shp.device is not None and shp.device.type == "cuda") else torch.device("cuda")
     cdt = _compute_dtype(shp, precision)
+    with torch.cuda.device(device):
+        return _attention_on_device(q, k, v, fq, fk, bias, mask, float(scale), cdt, split, shp, device, n, m, c)
+
+
+def _attention_on_device(q, k, v, fq, fk, bias, mask, scale, cdt, split, shp, device, n, m, c):
+    import torch
     qt = _to_torch(q, "q", device, cdt)
     kt = _to_torch(k, "k", device, cdt)
     vt = _to_torch(v, "v", device, cdt)
@@ -334,12 +450,17 @@ def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none",
         if tuple(bt.shape[-2:]) != (n, m):
             raise ShapeError(f"bias shape {tuple(bt.shape[-2:])} does not match logits {(n, m)}")
     mask_code = _lib.MASK_CODES[mask]
+    if qt.shape[0] * qt.shape[1] == 0:  # zero heads (e.g. an empty shard): nothing to launch
+        return _mirror(torch.empty(*qt.shape[:3], vt.shape[-1], dtype=qt.dtype, device=device), shp)
 
     if cdt == torch.float32:
+        if torch.is_grad_enabled() and _needs_grad(q, k, v, fq, fk, bias):
+            raise ConfigError("the fp32 path is forward-only: inputs that require grad need precision='bf16' "
+                              "or 'fp16' (tcgen05 forward + backward)")
         qf, kf, vf = (t.contiguous() for t in (qt, kt, vt))
         uq = uk = None
         if fqt is not None:
-            uq = (fqt.float() * premul).contiguous()
+            uq = (fqt.float() / scale).contiguous()
             uk = fkt.float().contiguous()
         bf = bt.float().contiguous() if bt is not None else None
         o, _ = _fwd_launch(qf, kf, vf, uq, uk, bf, mask_code, scale, need_lse=False)
@@ -348,6 +469,7 @@ def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none",
         qp, kp, vp = _pad_last(qt, dp), _pad_last(kt, dp), _pad_last(vt, dp)
         bp = None
         if bt is not None:
+            # -inf / finfo.min entries round to -inf: the kernels treat them as masked keys
             bt = bt.to(cdt)
             if m % 8:
                 store = torch.zeros(*bt.shape[:-1], (m + 7) // 8 * 8, dtype=cdt, device=device)
@@ -355,10 +477,17 @@ def _attention(q, k, v, *, fq=None, fk=None, premul=1.0, bias=None, mask="none",
                 bp = store[..., :m]
             else:
                 bp = bt.contiguous()
-        sp = None
+        kscale, premul, sp = scale, 1.0 / scale, None
         if fqt is not None:
-            sp = split or choose_split_cached(fqt, fkt, premul, max_cols=64 if dp == 128 else 128)
-        o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(scale), float(premul), sp)
+            max_cols = 64 if dp == 128 else 128
+            if split is not None:
+                plan = FactorPlan(int(split), False, 1.0 / scale, scale)
+            else:
+                plan = plan_factor_fold_cached(fq, fk, fqt, fkt, scale, max_cols=max_cols, panel_dtype=cdt)
+            sp, premul, kscale = plan.split, plan.premul, plan.kernel_scale
+            if plan.q_fold:  # Q' = [scale*q, U]: autograd carries d/dq = scale * d/dQ'
+                qp = qp * scale
+        o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(kscale), float(premul), sp)
         o = o[..., : vt.shape[-1]]
     return _mirror(o, shp)
 
@@ -388,9 +517,8 @@ def flashbias_attention(q, k, v, fq, fk, mask: str = MASK_NONE, tiles: Optional[
     the original 1/sqrt(C) scale, folded into the tcgen05 kernel."""
     _check_tiles(tiles)
     c = int(q.shape[-1])
-    root_c = math.sqrt(c)
-    return _attention(q, k, v, fq=fq, fk=fk, premul=root_c, mask=mask, scale=1.0 / root_c,
-                      precision=precision, split=split)
+    return _attention(q, k, v, fq=fq, fk=fk, mask=mask, scale=1.0 / math.sqrt(c), precision=precision,
+                      split=split)
 
 
 def tiled_attention(q, k, v, bias=NO_BIAS, mask: str = MASK_NONE, tiles: Optional[TileConfig] = None,
@@ -406,9 +534,9 @@ def tiled_attention(q, k, v, bias=NO_BIAS, mask: str = MASK_NONE, tiles: Optiona
     if isinstance(bias, DenseBias):
         return _attention(q, k, v, bias=bias.b, mask=mask, scale=scale, precision=precision)
     if isinstance(bias, FactoredBias):
-        # the factor term is added unscaled: uq = fq / scale so scale*uq.uk = fq.fk
-        return _attention(q, k, v, fq=bias.fq, fk=bias.fk, premul=1.0 / scale, mask=mask, scale=scale,
-                          precision=precision, split=split)
+        # the factor term is added unscaled: logits = scale*q.k + fq.fk
+        return _attention(q, k, v, fq=bias.fq, fk=bias.fk, mask=mask, scale=scale, precision=precision,
+                          split=split)
     raise ValidationError(f"unknown bias provider {type(bias).__name__}")
 
 

@@ -39,12 +39,9 @@
 #ifndef T128_REG_OT
 #define T128_REG_OT 72
 #endif
-#ifndef T128_DRAIN_MODE
-#define T128_DRAIN_MODE 0  // 0 = TMA reduce-add from a swizzled smem stage (4 = per-warp 2 KB boxes, no
-                           // cross-warp barriers: measured equal), 3 = red.global.add.v4.f32 after a
-                           // per-warp smem transpose (measured C3 bwd 25.1-25.4 ms vs 23.1 for mode 0);
-                           // experiments: 1 = TMA store (wrong), 2 = no global write
-#endif
+// dQ drain: TMA reduce-add from a swizzled smem stage.  Measured alternatives: per-warp
+// 2 KB boxes without cross-warp barriers (equal), red.global.add.v4.f32 after a per-warp smem transpose
+// (C3 bwd 25.1-25.4 ms vs 23.1), plain TMA stores (same time).
 #ifndef T128_QCHUNK
 #define T128_QCHUNK 16  // queries per dQ reduce-add box (16 KB of stages: 16 -> 2 x 8 KB SW64, 8 -> 4 x 4 KB SW32)
 #endif
@@ -418,99 +415,6 @@ __global__ void __launch_bounds__(512, 1)
     const int dd = threadIdx.x - 256;  // head-dim index = TMEM lane of dQ^T
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const bool leader = dd == 0;
-#if T128_DRAIN_MODE == 3
-    // Per-warp transpose through a private 4 KB scratch (rows = this warp's 32
-    // head dims, 16-byte chunks XOR-swizzled by row), then coalesced
-    // red.global.add.v4.f32: each instruction adds 4 rows x 32 queries (512 B).
-    // No TMA stage to wait on: the scratch is reused as soon as the warp has
-    // read it back, so reductions stay in flight in the memory system.
-    float* acc_bh = p.dq_acc + static_cast<int64_t>(b * p.H + h) * 128 * p.acc_n4;
-    uint8_t* scratch = reinterpret_cast<uint8_t*>(dq_stage) + (warp & 3) * 4096;
-    const int wrow0 = (warp & 3) * 32;
-    for (int j = 0; j < nblk; ++j) {
-      const int q0 = (i_start + j) * 128;
-      mbar_wait(&bars->dq_full, j & 1);
-      tc_fence_after();
-      if (leader) trace(p.trace, p.trace_cta, 19, j);
-      uint32_t v[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tmem_ld32(tmem + lane_off + T_DP + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->dq_free);
-      const float sc = p.scale;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {  // 32-query rounds
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          const int e = 32 * c + 4 * ch;
-          *reinterpret_cast<float4*>(scratch + lane * 128 + ((ch ^ (lane & 7)) << 4)) =
-              make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
-                          __uint_as_float(v[e + 3]) * sc);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int row = 4 * i + (lane >> 3), ch = lane & 7;
-          const float4 x = *reinterpret_cast<const float4*>(scratch + row * 128 + ((ch ^ (row & 7)) << 4));
-          const int q = q0 + 32 * c + 4 * ch;
-          if (q < p.N) {
-            float* dst = acc_bh + static_cast<int64_t>(wrow0 + row) * p.acc_n4 + q;
-            asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(x.x), "f"(x.y), "f"(x.z),
-                         "f"(x.w)
-                         : "memory");
-          }
-        }
-        __syncwarp();
-      }
-      if (leader) trace(p.trace, p.trace_cta, 20, j);
-    }
-#elif T128_DRAIN_MODE == 4
-    // Per-warp staging, no cross-warp barriers: warp w stages its 32 head-dim
-    // rows x 16 queries (2 KB, SW64) and its elected lane issues that box's
-    // reduce-add; two 2 KB stages per warp.
-    uint8_t* wst = reinterpret_cast<uint8_t*>(dq_stage) + (warp & 3) * 4096;
-    const int wrow0 = (warp & 3) * 32;
-    int chunk = 0;
-    for (int j = 0; j < nblk; ++j) {
-      const int q0 = (i_start + j) * 128;
-      mbar_wait(&bars->dq_full, j & 1);
-      tc_fence_after();
-      if (leader) trace(p.trace, p.trace_cta, 19, j);
-      uint32_t v[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        tmem_ld32(tmem + lane_off + T_DP + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * c));
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars->dq_free);
-      const float sc = p.scale;
-#pragma unroll
-      for (int c = 0; c < 8; ++c, ++chunk) {
-        uint8_t* stg = wst + (chunk & 1) * 2048;
-        if (lane == 0) t128_wait_read<1>();
-        __syncwarp();
-#pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          const int e = 16 * c + 4 * c4;
-          *reinterpret_cast<float4*>(stg + lane * 64 + ((c4 ^ ((lane >> 1) & 3)) << 4)) =
-              make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
-                          __uint_as_float(v[e + 3]) * sc);
-        }
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) {
-          t128_reduce_add(&tm_dqacc, stg, q0 + 16 * c, wrow0, h, b);
-          t128_bulk_commit();
-        }
-      }
-      if (leader) trace(p.trace, p.trace_cta, 20, j);
-    }
-    if (lane == 0) t128_wait_all();
-#else
     int chunk = 0;
     for (int j = 0; j < nblk; ++j) {
       const int q0 = (i_start + j) * 128;
@@ -542,19 +446,12 @@ __global__ void __launch_bounds__(512, 1)
         fence_proxy_async();
         named_bar_sync(3, 128);
         if (leader) {
-#if T128_DRAIN_MODE == 0
           t128_reduce_add(&tm_dqacc, stg, q0 + QC * c, 0, h, b);
-#elif T128_DRAIN_MODE == 1
-          asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                           reinterpret_cast<uint64_t>(&tm_dqacc)), "r"(smem_u32(stg)), "r"(q0 + QC * c), "r"(0),
-                       "r"(h), "r"(b) : "memory");
-#endif
           t128_bulk_commit();
         }
       }
       if (leader) trace(p.trace, p.trace_cta, 20, j);
     }
-#endif
     if (leader) t128_wait_all();
   }
 
@@ -624,8 +521,8 @@ cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, 
   return cudaGetLastError();
 }
 
-int bwd_t128_qchunk() { return T128_DRAIN_MODE == 4 ? 16 : T128_QCHUNK; }
-int bwd_t128_box_rows() { return T128_DRAIN_MODE == 4 ? 32 : 128; }
+int bwd_t128_qchunk() { return T128_QCHUNK; }
+int bwd_t128_box_rows() { return 128; }
 
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads) {
   return d == 128 && rp <= 1 && !dense && !factor_grads;

@@ -13,6 +13,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 
 #include "../../include/flashbias_b200.h"
@@ -22,9 +23,10 @@
 namespace fb {
 
 static thread_local char g_err[512] = "";
-static thread_local int64_t g_launches = 0;
+// process-wide (autograd runs the backward on its own thread)
+static std::atomic<int64_t> g_launches{0};
 
-void note_launch(int n) { g_launches += n; }
+void note_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static unsigned long long* g_trace_buf = nullptr;
 static int g_trace_cta = -1;
@@ -195,9 +197,7 @@ void fb_debug_set_trace(void* buf, int cta) {
 int fb_debug_trace_enabled(void) { return FB_TRACE; }
 int fb_abi_version(void) { return FB_ABI_VERSION; }
 int64_t fb_launch_count(int reset) {
-  const int64_t c = g_launches;
-  if (reset) g_launches = 0;
-  return c;
+  return reset ? g_launches.exchange(0, std::memory_order_relaxed) : g_launches.load(std::memory_order_relaxed);
 }
 
 int64_t fb_factor_cols(int64_t rank, int split) { return rank * factor_pairs(split); }
@@ -217,6 +217,7 @@ int fb_attn_fwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     return fail(FB_ESHAPE, "output shape mismatch");
   if (o->dtype != q->dtype) return fail(FB_EVALUE, "output dtype must match q");
   if (!(scale > 0.f) || !isfinite(scale)) return fail(FB_EVALUE, "scale must be positive and finite");
+  if (q->shape[0] * q->shape[1] == 0) return FB_OK;  // no heads: nothing to launch
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int B = (int)q->shape[0], H = (int)q->shape[1], N = (int)q->shape[2], M = (int)k->shape[2];
   const int D = (int)q->shape[3];
@@ -333,6 +334,7 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
   const int B = (int)q->shape[0], H = (int)q->shape[1], N = (int)q->shape[2], M = (int)k->shape[2];
   const int D = (int)q->shape[3];
   if (D != 32 && D != 64 && D != 128) return fail(FB_ECONFIG, "backward supports head dim 32, 64, 128");
+  if (q->shape[0] * q->shape[1] == 0) return FB_OK;  // no heads: nothing to launch
   if (workspace_bytes < fb_bwd_workspace_bytes(q, k) || !workspace) return fail(FB_ECONFIG, "workspace too small");
   int rp = 0;
   if (uq) {

@@ -390,7 +390,10 @@ __global__ void __launch_bounds__(384, 1)
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       {
         const float2 mul = DENSE ? make_float2(1.f, 1.f) : make_float2(sl2, sl2);
-        const float2 neg = make_float2(-m_run, -m_run);
+        // a row whose keys so far are all -inf (dense bias masking whole trailing key
+        // blocks, visited first) has m_run = -inf: subtract 0 so p = 2^-inf = 0, not NaN
+        const float m_use = m_run == -INFINITY ? 0.f : m_run;
+        const float2 neg = make_float2(-m_use, -m_use);
         uint32_t pk[64];
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
@@ -448,7 +451,8 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     if (valid && p.lse != nullptr) {
-      const float lse = (m_run + __log2f(l_run)) * 0.6931471805599453f;
+      // fully masked row: LSE = +inf makes the backward's p = exp(s - lse) exactly 0
+      const float lse = l_run > 0.f ? (m_run + __log2f(l_run)) * 0.6931471805599453f : INFINITY;
       p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + row] = lse;
     }
   }

@@ -7,6 +7,9 @@ import bench
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"]
 inp = bench.make_inputs(cfg, 0, cfg["H"], torch.device("cuda"))
 import paper_2505_12044_b200 as fb
+from paper_2505_12044_b200 import _lib
+if os.environ.get("FLASHBIAS_B200_VARIANT"):  # probe only: load _lib/libflashbias_b200_<name>.so
+    _lib.LIB_PATH = os.path.join(os.path.dirname(_lib.LIB_PATH), "libflashbias_b200_%s.so" % os.environ["FLASHBIAS_B200_VARIANT"])
 mask = "causal" if cfg["causal"] else "none"
 q, k, v = inp["q"], inp["k"], inp["v"]
 def fwd():

@@ -1,11 +1,11 @@
 """Timeline of one CTA of the fwd and fused bwd kernels (FB_TRACE build).
 python tests/gpu_probe/trace_run.py [cta] [H]"""
 import ctypes, os, sys, collections
-os.environ["FLASHBIAS_B200_TRACE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2505_12044_b200 as fb
 from paper_2505_12044_b200 import _lib
+_lib.LIB_PATH = os.path.join(os.path.dirname(_lib.LIB_PATH), "libflashbias_b200_trace.so")  # debug build
 lib = _lib.lib()
 lib.fb_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 40

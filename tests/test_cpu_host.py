@@ -150,3 +150,75 @@ def test_flashbias_alias_package():
     import flashbias
     assert flashbias.flashbias_attention is fb.flashbias_attention
     assert set(["flashbias_attention", "tiled_attention", "svd_decompose", "decompose_alibi"]) <= set(flashbias.__all__)
+
+
+def test_choose_split_raises_instead_of_dropping_below_its_bound():
+    """R=64 factors premultiplied by sqrt(128) cannot meet
+    1e-2 logits inside 64 panel columns -> ConfigError, never a silent k=1."""
+    torch = pytest.importorskip("torch")
+    g = torch.Generator().manual_seed(0)
+    fq = (torch.randn(1, 1, 512, 64, generator=g) / 8).bfloat16().float()
+    fk = torch.randn(1, 1, 512, 64, generator=g).bfloat16().float()
+    with pytest.raises(ConfigError):
+        fb.choose_split(fq, fk, premul=128 ** 0.5, max_cols=64)
+    assert fb.choose_split(fq, fk, premul=1.0, max_cols=64) == 1
+
+
+def test_factor_fold_plan():
+    """north_star fold Q' = [scale*q, U] is chosen exactly when the reference
+    order's sqrt(C) premultiplier would cost split columns."""
+    torch = pytest.importorskip("torch")
+    from paper_2505_12044_b200.attention import plan_factor_fold
+    g = torch.Generator().manual_seed(1)
+    fq = (torch.randn(1, 1, 256, 64, generator=g) / 8).bfloat16().float()
+    fk = torch.randn(1, 1, 256, 64, generator=g).bfloat16().float()
+    # d=128: 1/scale = sqrt(128) inexact -> Q' fold, no split
+    p = plan_factor_fold(fq, fk, 128 ** -0.5, max_cols=64)
+    assert p.q_fold and p.split == 1 and p.premul == 1.0 and p.kernel_scale == 1.0
+    # d=64: sqrt(64) = 8 is a power of two -> reference order, exact, no split
+    p = plan_factor_fold(fq, fk, 64 ** -0.5, max_cols=128)
+    assert not p.q_fold and p.split == 1 and p.premul == 8.0
+    # ALiBi at N=16384 needs the 3-way split either way -> reference order (no extra pass over q)
+    i = torch.arange(1, 16385, dtype=torch.float32)
+    s = -(2.0 ** (-8 / 32 * 3))
+    fa = torch.stack([torch.full_like(i, s), s * i], -1)[None, None]
+    fb_ = torch.stack([-i, torch.ones_like(i)], -1)[None, None]
+    p = plan_factor_fold(fa, fb_, 128 ** -0.5, max_cols=64)
+    assert not p.q_fold and p.split == 3
+    # nothing fits -> ConfigError
+    big = torch.randn(1, 1, 64, 64, generator=g) * 1e4
+    with pytest.raises(ConfigError):
+        plan_factor_fold(big, big, 128 ** -0.5, max_cols=64)
+
+
+def test_split_cache_checks_object_identity():
+    """a new factor tensor that reuses a freed allocation must not
+    inherit the cached plan of the old one."""
+    torch = pytest.importorskip("torch")
+    from paper_2505_12044_b200 import attention as A
+    A._SPLIT_CACHE.clear()
+    fq = torch.ones(1, 1, 64, 2)
+    fk = torch.ones(1, 1, 64, 2)
+    p1 = A.plan_factor_fold_cached(fq, fk, fq, fk, 0.125, tol=1e-6)
+    assert p1.split == 1
+    fq2 = torch.full((1, 1, 64, 2), 1.0 + 2.0 ** -12)  # inexact in bf16: 2.4e-4 per rank at k=1
+    fk2 = fk.clone()
+    p2 = A.plan_factor_fold_cached(fq2, fk2, fq2, fk2, 0.125, tol=1e-6)
+    assert p2.split > 1
+    fq.mul_(1.0 + 2.0 ** -12)  # in-place write bumps the version -> re-planned
+    assert A.plan_factor_fold_cached(fq, fk, fq, fk, 0.125, tol=1e-6).split > 1
+
+
+def test_core_helpers_match_reference_semantics():
+    a, b = np.arange(6.0).reshape(2, 3), np.ones((2, 2))
+    assert fb.concat_cols(a, b).shape == (2, 5)
+    with pytest.raises(ShapeError):
+        fb.concat_cols(a, np.ones((3, 2)))
+    with pytest.raises(ShapeError):
+        fb.matmul(a, a)
+    assert fb.matmul(a, a.T).shape == (2, 2)
+    s = fb.softmax_rows(np.array([[1e300, 0.0], [0.0, 0.0]]))
+    assert np.allclose(s, [[1.0, 0.0], [0.5, 0.5]])
+    assert abs(fb.frobenius(np.array([[3.0, 4.0]])) - 5.0) < 1e-15
+    with pytest.raises(ShapeError):
+        fb.frobenius(np.ones(3))

@@ -1,0 +1,167 @@
+"""Parity at the BASELINE config sizes: full-length heads
+of C2, C3, C4 and C5 through the public API, forward and backward, against
+the float64 oracle (oracle/flashbias_oracle.py, pinned to the reference's own
+outputs by tests/test_oracle_golden.py) on the same bf16-rounded inputs.
+
+Tolerance (north_star): bf16 2e-2 relative, metric max|got - ref| / max|ref|
+per head and per tensor.  The oracle streams each head over
+query blocks (blocked_attention_fwd_bwd) so a 16384-key head fits in memory.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import bench
+import paper_2505_12044_b200 as fb
+from oracle import flashbias_oracle as orc
+from paper_2505_12044_b200 import attention as A
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+def _rand(shape, seed, dtype=torch.bfloat16):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn(*shape, generator=g, device="cuda").to(dtype)
+
+
+def _np(t):
+    return t.detach().double().cpu().numpy()
+
+
+def _check_head(got: dict, ref: dict, keys, what: str):
+    errs = {key: orc.rel_max_err(got[key], ref[key]) for key in keys}
+    bad = {k_: e for k_, e in errs.items() if not e < TOL}
+    assert not bad, f"{what}: {errs}"
+    return errs
+
+
+def _run(q, k, v, do, fq, fk, mask, learn_factors=False):
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    if learn_factors:
+        fq.requires_grad_(True)
+        fk.requires_grad_(True)
+    o = fb.flashbias_attention(q, k, v, fq, fk, mask=mask)
+    wrt = (q, k, v, fq, fk) if learn_factors else (q, k, v)
+    grads = torch.autograd.grad(o, wrt, do)
+    names = ("dq", "dk", "dv", "dfq", "dfk")[: len(grads)]
+    return dict(o=o.detach(), **dict(zip(names, grads)))
+
+
+def test_c3_full_heads_causal_alibi_three_way_split():
+    """C3: N=16384, d=128, causal, the steepest standard slope -2^-0.25 (3-way
+    bf16 split, factor magnitudes ~1.5e5 after the sqrt(128) premultiply) on two
+    batch rows sharing the factors, plus the flattest slope; fwd + the
+    128x128-tile backward (the C3 production kernels)."""
+    N, H, d = 16384, 32, 128
+    slopes = bench.alibi_slopes(H)
+    for h, B in ((0, 2), (31, 1)):
+        q, k, v, do = (_rand((B, 1, N, d), 100 * h + i) for i in range(4))
+        fq, fk = fb.alibi_factors([slopes[h]], N, N)  # [1, 1, N, 2], broadcast over the batch
+        plan = A.plan_factor_fold(fq, fk, 1 / math.sqrt(d))
+        if h == 0:
+            assert plan.split == 3 and not plan.q_fold
+        got = _run(q, k, v, do, fq, fk, "causal")
+        fq64, fk64 = orc.decompose_alibi(N, N, slopes[h])
+        for b in range(B):
+            ref = orc.blocked_attention_fwd_bwd(_np(q[b, 0]), _np(k[b, 0]), _np(v[b, 0]), _np(do[b, 0]),
+                                                fq=fq64, fk=fk64, premul=math.sqrt(d), mask="causal",
+                                                scale=1 / math.sqrt(d), block=2048)
+            _check_head({key: _np(t[b, 0]) for key, t in got.items()}, ref, ("o", "dq", "dk", "dv"),
+                        f"C3 head {h} batch {b}")
+
+
+def test_c2_full_heads_spatial_grid_learnable_weights():
+    """C2: the real 64x64 grid (N=4096), d=64, 2-way split of the rank-9
+    spatial factors, learnable per-head row weights: dfq/dfk through the fused
+    d=64 backward with factor gradients."""
+    N, d, heads = 4096, 64, (0, 5, 11)
+    side = 64
+    r = torch.arange(N, device="cuda") // side
+    c = torch.arange(N, device="cuda") % side
+    pos = torch.stack([r / (side - 1), c / (side - 1), torch.zeros(N, device="cuda")], -1).float()
+    w = torch.stack([-(0.5 + 1.5 * torch.as_tensor(fb.Rng(2000 + h).uniform(N), device="cuda").float())
+                     for h in heads])
+    fq, fk = fb.spatial_factors(pos, pos, w[None])  # [1, Hs, N, 9], [1, 1, N, 9]
+    fk = fk.expand(1, len(heads), N, 9).contiguous()
+    fq, fk = fq.detach().clone(), fk.detach().clone()
+    q, k, v, do = (_rand((1, len(heads), N, d), 7 + i) for i in range(4))
+    got = _run(q, k, v, do, fq, fk, "none", learn_factors=True)
+    for i in range(len(heads)):
+        ref = orc.blocked_attention_fwd_bwd(_np(q[0, i]), _np(k[0, i]), _np(v[0, i]), _np(do[0, i]),
+                                            fq=_np(fq[0, i]), fk=_np(fk[0, i]), premul=math.sqrt(d),
+                                            scale=1 / math.sqrt(d), block=2048)
+        _check_head({key: _np(t[0, i]) for key, t in got.items()}, ref, ("o", "dq", "dk", "dv", "dfq", "dfk"),
+                    f"C2 head {heads[i]}")
+
+
+@pytest.mark.parametrize("learn", [False, True])
+def test_c5_full_head_rank64_svd_factors(learn):
+    """C5: N=8192, d=128, R=64 factors from the device randomized SVD of the
+    §8(d) dense bias (4 factor panels); static factors take the 64-query fused
+    backward, learnable ones the two-kernel backward with dfq/dfk."""
+    N, d = 8192, 128
+    b = bench.c5_bias(N, 5000, "cuda")
+    fac, rep = fb.svd_decompose(b, rank=64)
+    fq, fk = fac.fq.float().contiguous()[None, None], fac.fk.float().contiguous()[None, None]
+    assert rep.rank_used == 64 and rep.rel_fro_err < 1e-2
+    q, k, v, do = (_rand((1, 1, N, d), 50 + i) for i in range(4))
+    got = _run(q, k, v, do, fq, fk, "none", learn_factors=learn)
+    ref = orc.blocked_attention_fwd_bwd(_np(q[0, 0]), _np(k[0, 0]), _np(v[0, 0]), _np(do[0, 0]),
+                                        fq=_np(fq[0, 0]), fk=_np(fk[0, 0]), premul=math.sqrt(d),
+                                        scale=1 / math.sqrt(d), block=2048)
+    keys = ("o", "dq", "dk", "dv") + (("dfq", "dfk") if learn else ())
+    _check_head({key: _np(t[0, 0]) for key, t in got.items()}, ref, keys, f"C5 learn={learn}")
+
+
+@pytest.mark.parametrize("rank", [16, 32])
+def test_c4_af3_pair_bias_svd_and_attention(rank):
+    """C4: the AF3-style pair bias (N=768, H=16, d=32): device svd_decompose
+    against the oracle's LAPACK SVD (rank, energy, errors), then attention with
+    the device factors against the oracle, forward and backward."""
+    N, H, d = 768, 16, 32
+    bias = bench.af3_pair_bias(N, range(H), "cuda")
+    fqs, fks = [], []
+    for h in range(H):
+        fac, rep = fb.svd_decompose(bias[h], rank=rank)
+        ofq, ofk, orep = orc.svd_decompose(bias[h].cpu().numpy(), rank=rank)
+        assert rep.rank_used == orep["rank_used"] == rank
+        assert abs(rep.energy_retained - orep["energy_retained"]) < 1e-9
+        assert abs(rep.max_abs_err - orep["max_abs_err"]) <= 1e-6 * max(orep["max_abs_err"], 1e-12) + 1e-12
+        assert abs(rep.rel_fro_err - orep["rel_fro_err"]) <= 1e-6 * max(orep["rel_fro_err"], 1e-12) + 1e-12
+        fqs.append(fac.fq)
+        fks.append(fac.fk)
+    fq = torch.stack(fqs)[None].float().contiguous()
+    fk = torch.stack(fks)[None].float().contiguous()
+    q, k, v, do = (_rand((1, H, N, d), 70 + i) for i in range(4))
+    got = _run(q, k, v, do, fq, fk, "none", learn_factors=True)
+    for h in range(H):
+        ref = orc.blocked_attention_fwd_bwd(_np(q[0, h]), _np(k[0, h]), _np(v[0, h]), _np(do[0, h]),
+                                            fq=_np(fq[0, h]), fk=_np(fk[0, h]), premul=math.sqrt(d),
+                                            scale=1 / math.sqrt(d))
+        _check_head({key: _np(t[0, h]) for key, t in got.items()}, ref, ("o", "dq", "dk", "dv", "dfq", "dfk"),
+                    f"C4 R={rank} head {h}")
+
+
+def test_dense_bias_masking_trailing_key_blocks_is_finite():
+    """a dense bias whose last >= 128 keys are -inf (key
+    padding) must not turn the reverse-order forward into NaN."""
+    N, M, d = 256, 512, 64
+    q, k, v, do = _rand((1, 2, N, d), 1), _rand((1, 2, M, d), 2), _rand((1, 2, M, d), 3), _rand((1, 2, N, d), 4)
+    bias = torch.zeros(1, 2, N, M, device="cuda")
+    bias[..., 300:] = float("-inf")
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    o = fb.tiled_attention(q, k, v, fb.DenseBias(bias))
+    dq, dk, dv = torch.autograd.grad(o, (q, k, v), do)
+    assert torch.isfinite(o).all() and torch.isfinite(dq).all() and torch.isfinite(dk).all()
+    for h in range(2):
+        ref = orc.attention_bwd(_np(q[0, h]), _np(k[0, h]), _np(v[0, h]), _np(do[0, h]), bias=_np(bias[0, h]))
+        _check_head({"o": _np(o[0, h]), "dq": _np(dq[0, h]), "dk": _np(dk[0, h]), "dv": _np(dv[0, h])}, ref,
+                    ("o", "dq", "dk", "dv"), f"masked dense head {h}")
+    assert float(dk[..., 300:, :].abs().max()) == 0.0 and float(dv[..., 300:, :].abs().max()) == 0.0

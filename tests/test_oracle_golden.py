@@ -146,3 +146,17 @@ def test_backward_oracle_finite_differences():
             dn[idx][i] -= 1e-6
             num[i] = (loss(*up) - loss(*dn)) / 2e-6
         assert np.abs(num - g[name]).max() <= 1e-7, name
+
+
+def test_blocked_fwd_bwd_matches_materialised_backward():
+    """The config-size GPU parity tests use the query-blocked restatement;
+    it must equal attention_bwd (materialised) to rounding."""
+    rng = np.random.default_rng(3)
+    for mask in ("none", "causal"):
+        n, d, r = 300, 16, 3
+        q, k, v, do = (rng.standard_normal((n, d)) for _ in range(4))
+        fq, fk = rng.standard_normal((n, r)), rng.standard_normal((n, r))
+        a = orc.attention_bwd(q, k, v, do, fq=fq, fk=fk, premul=4.0, mask=mask)
+        b = orc.blocked_attention_fwd_bwd(q, k, v, do, fq=fq, fk=fk, premul=4.0, mask=mask, block=64)
+        for key in ("o", "dq", "dk", "dv", "dfq", "dfk"):
+            assert orc.rel_max_err(b[key], a[key]) < 1e-12, (mask, key)

@@ -51,9 +51,19 @@ def _worker(rank, world, port, result_path):
     lo, hi = head_range(H, world, rank)
     part = torch.full((B, hi - lo, 2), float(rank))
     allp = gather_heads(part, H)
+    # chunked compute + gather (slices land in place by per-rank broadcasts) == unchunked
+    chunked = sharded_apply(hot, [q, k, v, fq, fk], H, chunks=2)
+    # a 2-D [N, R] factor with R == H is shared, never split by columns
+    shared = torch.randn(N, H, generator=g, dtype=torch.float64)
+    got2d = sharded_apply(lambda a, f: a.sum(-1, keepdim=True) + f.sum(), [q, shared], H)
+    # H < world: the empty rank still takes part in the gather
+    one = sharded_apply(lambda a: a * 2, [q[:, :1]], 1)
     if rank == 0:
         res = torch.load(result_path)
         res["ragged"] = allp[0, :, 0].tolist()
+        res["chunked_eq"] = bool(torch.equal(chunked, full))
+        res["shared_eq"] = bool(torch.equal(got2d, q.sum(-1, keepdim=True) + shared.sum()))
+        res["one_eq"] = bool(torch.equal(one, q[:, :1] * 2))
         torch.save(res, result_path)
     dist.barrier()
     dist.destroy_process_group()
@@ -65,3 +75,4 @@ def test_sharded_equals_unsharded_gloo(tmp_path):
     res = torch.load(path)
     assert res["eq"] and res["shape"] == (2, 5, 40, 8)
     assert res["ragged"] == [0.0, 0.0, 0.0, 1.0, 1.0]
+    assert res["chunked_eq"] and res["shared_eq"] and res["one_eq"]
