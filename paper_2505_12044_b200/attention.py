@@ -269,26 +269,35 @@ def plan_factor_fold(fq, fk, scale: float, tol: float = 1e-2, max_cols: int = 64
         f"or use the fp32 path")
 
 
+def _base_of(t):
+    return t._base if t._base is not None else t
+
+
 def plan_factor_fold_cached(fq_user, fk_user, fq, fk, scale: float, tol: float = 1e-2,
                             max_cols: int = 64, panel_dtype=None) -> FactorPlan:
-    """plan_factor_fold memoised per user factor OBJECTS (the decision needs a
-    device->host read; static factors such as ALiBi/spatial pay it once).  The
-    entry is reused only while weak references still resolve to the very same
-    tensors at the same in-place version, so a new tensor that happens to reuse
-    a freed allocation never inherits a stale split level.  numpy inputs (a
-    fresh device copy every call) are not cached."""
+    """plan_factor_fold memoised per user factor tensors (the decision needs a
+    device->host read; static factors such as ALiBi/spatial pay it once).
+
+    Identity = the base tensor OBJECT (held by weak reference) + the view
+    geometry + the shared in-place version counter, so per-call views of the
+    same factors (head slices) hit the cache, while a new tensor that happens
+    to reuse a freed allocation never inherits a stale split level.  numpy
+    inputs (a fresh device copy every call) are not cached."""
     import weakref
     if not (_is_torch(fq_user) and _is_torch(fk_user)):
         return plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype)
-    key = (id(fq_user), id(fk_user), fq_user._version, fk_user._version, float(scale), float(tol), int(max_cols),
-           str(panel_dtype))
+    bq, bk = _base_of(fq_user), _base_of(fk_user)
+
+    def geom(t, base):
+        return (id(base), base._version, t.storage_offset(), tuple(t.shape), tuple(t.stride()), t.dtype)
+    key = (geom(fq_user, bq), geom(fk_user, bk), float(scale), float(tol), int(max_cols), str(panel_dtype))
     hit = _SPLIT_CACHE.get(key)
-    if hit is not None and hit[0]() is fq_user and hit[1]() is fk_user:
+    if hit is not None and hit[0]() is bq and hit[1]() is bk:
         return hit[2]
     plan = plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype)
     if len(_SPLIT_CACHE) > 256:
         _SPLIT_CACHE.clear()
-    _SPLIT_CACHE[key] = (weakref.ref(fq_user), weakref.ref(fk_user), plan)
+    _SPLIT_CACHE[key] = (weakref.ref(bq), weakref.ref(bk), plan)
     return plan
 
 

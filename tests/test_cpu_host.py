@@ -207,6 +207,12 @@ def test_split_cache_checks_object_identity():
     assert p2.split > 1
     fq.mul_(1.0 + 2.0 ** -12)  # in-place write bumps the version -> re-planned
     assert A.plan_factor_fold_cached(fq, fk, fq, fk, 0.125, tol=1e-6).split > 1
+    # views of the same factors (per-call head slices) hit the cache
+    fq3, fk3 = torch.full((1, 3, 64, 2), 1.0 + 2.0 ** -12), torch.ones(1, 3, 64, 2)
+    n0 = len(A._SPLIT_CACHE)
+    for _ in range(3):
+        A.plan_factor_fold_cached(fq3[:, 1:2], fk3[:, 1:2], fq3[:, 1:2], fk3[:, 1:2], 0.125, tol=1e-6)
+    assert len(A._SPLIT_CACHE) == n0 + 1
 
 
 def test_core_helpers_match_reference_semantics():
