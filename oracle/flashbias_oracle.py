@@ -56,11 +56,12 @@ def materialized_attention(q, k, v, fq=None, fk=None, premul=1.0, bias=None, mas
 
 
 def streaming_attention(q, k, v, fq=None, fk=None, premul=1.0, bias=None, mask="none", scale=None,
-                        block_q=128, block_kv=128):
+                        block_q=128, block_kv=128, row0=0):
     """Online-softmax streaming loop (ref: attention.py:140-202, hot loop 174-201).
 
     Returns (O, LSE) with LSE = logsumexp of the masked logits per row.
     Causal key blocks entirely above the diagonal are skipped (ref: 184-185).
+    ``row0``: global index of q's first row (a row sample of a causal head).
     """
     q, k, v = (np.asarray(x, dtype=np.float64) for x in (q, k, v))
     fq = None if fq is None else np.asarray(fq, dtype=np.float64)
@@ -74,20 +75,20 @@ def streaming_attention(q, k, v, fq=None, fk=None, premul=1.0, bias=None, mask="
     cols = np.arange(m)
     for q0 in range(0, n, block_q):
         q1 = min(q0 + block_q, n)
-        rows = np.arange(q0, q1)
+        rows = np.arange(q0, q1) + row0
         mx = np.full(lead + (q1 - q0,), -np.inf)
         den = np.zeros(lead + (q1 - q0,))
         acc = np.zeros(lead + (q1 - q0, v.shape[-1]))
         for k0 in range(0, m, block_kv):
             k1 = min(k0 + block_kv, m)
-            if mask == "causal" and k0 > q1 - 1:
+            if mask == "causal" and k0 > row0 + q1 - 1:
                 break
             s = np.einsum("...nc,...mc->...nm", q[..., q0:q1, :], k[..., k0:k1, :]) * scale
             if fq is not None:
                 s = s + np.einsum("...nr,...mr->...nm", premul * fq[..., q0:q1, :], fk[..., k0:k1, :]) * scale
             if bias is not None:
                 s = s + bias[..., q0:q1, k0:k1]
-            if mask == "causal" and k1 - 1 > q0:
+            if mask == "causal" and k1 - 1 > row0 + q0:
                 s = np.where(cols[None, k0:k1] > rows[:, None], MASK_FILL, s)
             m_new = np.maximum(mx, s.max(axis=-1))
             p = np.exp(s - m_new[..., None])
@@ -146,14 +147,16 @@ def attention_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, bias=None, mask="no
 
 
 def blocked_attention_fwd_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, mask="none", scale=None,
-                              block=1024):
+                              block=1024, row0=0):
     """attention_bwd for ONE 2-D head at full config size, streamed over query
     blocks so memory stays O(block * M) (a 16384^2 float64 logit matrix would
     be 2 GiB per array).  Same arithmetic as attention_bwd (its analytic
     gradient of ref attention.py:111-137 / 205-230), row block by row block:
     each block sees all the keys it can attend to, so its softmax, O rows, dS
     rows, dq rows and dfq rows are final and its dK, dV, dfk contributions are
-    summed.  Returns dict(o, lse, dq, dk, dv[, dfq, dfk])."""
+    summed.  ``row0``: global index of q's first row (q, do, fq may be a row
+    sample of the head; dk, dv, dfk are then that sample's contributions).
+    Returns dict(o, lse, dq, dk, dv[, dfq, dfk])."""
     q, k, v, do = (np.asarray(x, dtype=np.float64) for x in (q, k, v, do))
     scale = 1.0 / math.sqrt(q.shape[-1]) if scale is None else scale
     n, m = q.shape[0], k.shape[0]
@@ -166,12 +169,12 @@ def blocked_attention_fwd_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, mask="n
         res["dfq"], res["dfk"] = np.empty_like(fq), np.zeros_like(fk)
     for q0 in range(0, n, block):
         q1 = min(q0 + block, n)
-        m1 = min(m, q1) if mask == "causal" else m  # keys any row of the block can see
+        m1 = min(m, row0 + q1) if mask == "causal" else m  # keys any row of the block can see
         s = (q[q0:q1] @ k[:m1].T) * scale
         if fq is not None:
             s += (fq[q0:q1] @ fk[:m1].T) * scale
         if mask == "causal":
-            s[np.arange(m1)[None, :] > np.arange(q0, q1)[:, None]] = -np.inf
+            s[np.arange(m1)[None, :] > np.arange(row0 + q0, row0 + q1)[:, None]] = -np.inf
         mx = s.max(axis=1, keepdims=True)
         p = np.exp(s - mx)
         den = p.sum(axis=1, keepdims=True)
