@@ -282,174 +282,6 @@ def reference_svd_report(cfg, n_heads: int = 1):
     return t
 
 
-def peaks():
-    try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
-    except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
-
-
-# ---------------------------------------------------------------------------- clocks
-class ClockSampler:
-    """Poll SM clock / throttle reasons with NVML during the timed region."""
-
-    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
-               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-               0x100: "display_clock_setting"}
-
-    def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
-        self._stop = threading.Event()
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:  # noqa: BLE001
-            self.nv = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:  # noqa: BLE001
-                pass
-            time.sleep(0.05)
-
-    def __enter__(self):
-        if self.nv is not None:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
-        return self
-
-    def __exit__(self, *exc):
-        self._stop.set()
-        if self.nv is not None:
-            self.t.join()
-
-    def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
-
-
-# ---------------------------------------------------------------------------- GPU arm
-def make_inputs(cfg, h_lo: int, h_hi: int, device, seed: int = 1234):
-    """Synthetic inputs for heads [h_lo, h_hi) and all B batch rows, q/k/v/dO
-    [B, H_loc, N, d] seeded per (b, h) with seed + b*H + h, so any head
-    sharding sees identical per-head data."""
-    import torch
-
-    import paper_2505_12044_b200 as fb
-    B, H, N, d = cfg["B"], cfg["H"], cfg["N"], cfg["d"]
-    dt = torch.float32 if cfg["dtype"] == "fp32" else torch.bfloat16
-    heads = list(range(h_lo, h_hi))
-    hl = len(heads)
-    q = torch.empty(B, hl, N, d, dtype=dt, device=device)
-    k, v, do = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
-    g = torch.Generator(device=device)
-    for b in range(B):
-        for i, h in enumerate(heads):
-            g.manual_seed(seed + b * H + h)
-            for t in (q, k, v, do):
-                t[b, i].normal_(generator=g)
-    fq = fk = None
-    if cfg["bias"] == "alibi":  # batch-broadcast factors [1, H_loc, N, 2]
-        slopes = [alibi_slopes(H)[h] for h in heads]
-        fq, fk = fb.alibi_factors(slopes, N, N)
-    elif cfg["bias"] == "spatial":  # learnable per-head row weights, shared positions
-        side = int(round(math.sqrt(N)))
-        r = torch.arange(N, device=device) // side
-        c = torch.arange(N, device=device) % side
-        pos = torch.stack([r / (side - 1), c / (side - 1), torch.zeros(N, device=device)], -1).float()
-        from paper_2505_12044_b200.rng import Rng
-        w = torch.stack([-(0.5 + 1.5 * torch.as_tensor(Rng(2000 + h).uniform(N), device=device).float())
-                         for h in heads])
-        fq, fk = fb.spatial_factors(pos, pos, w[None])  # fq [1,H_loc,N,9], fk [1,1,N,9]
-        fk = fk.expand(1, hl, N, 9).contiguous()
-    else:  # C4 / C5: dense biases factorised on the device (SVD), the north_star approximate path
-        fq, fk, fact = svd_factors(cfg, heads, device)
-        return dict(q=q, k=k, v=v, do=do, fq=fq, fk=fk, dense=None, heads=heads, factorisation=fact)
-    return dict(q=q, k=k, v=v, do=do, fq=fq, fk=fk, dense=None, heads=heads)
-
-
-def dense_biases(cfg, heads, device, b: int):
-    """The exact dense biases of batch row b for ``heads``: [len(heads), N, N] fp32 on device."""
-    import torch
-    if cfg["bias"] == "af3":
-        return af3_pair_bias(cfg["N"], heads, device).float()
-    return torch.stack([c5_bias(cfg["N"], 5000 + b * cfg["H"] + h, device) for h in heads])
-
-
-def svd_factors(cfg, heads, device):
-    """Device SVD of every (b, h) dense bias at rank R (C4: exact cuSOLVER SVD of the
-    shared pair bias, B=1; C5: batched randomized SVD per batch row) -> fp32
-    factors [B, H_loc, N, R] + the reconstruction report (ref decompose.py:98-165)."""
-    import torch
-
-    import paper_2505_12044_b200 as fb
-    from paper_2505_12044_b200.decompose import randomized_svd
-    B, N, R = cfg["B"], cfg["N"], int(cfg["R"])
-    fq = torch.empty(B, len(heads), N, R, device=device)
-    fk = torch.empty_like(fq)
-    worst = {"max_abs_err": 0.0, "rel_fro_err": 0.0, "energy_retained": 1.0}
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for b in range(B):
-        bias = dense_biases(cfg, heads, device, b)
-        if cfg["bias"] == "af3":  # exact SVD (cuSOLVER, fp64) per head, like the reference's dgesdd
-            u, s, vh = torch.linalg.svd(bias.double(), full_matrices=False)
-            u, s, vh = u[..., :R], s[..., :R], vh[..., :R, :]
-        else:  # randomized range finder (K7), batched over the heads of this batch row
-            u, s, vh = randomized_svd(bias, R)
-        root = s.sqrt()
-        fq[b] = (u * root[..., None, :]).float()
-        fk[b] = (vh.transpose(-1, -2) * root[..., None, :]).float()
-        diff = fq[b].double() @ fk[b].double().transpose(-1, -2) - bias.double()
-        nb = bias.double().pow(2).sum((-1, -2))
-        rel = (diff.pow(2).sum((-1, -2)) / nb).sqrt()
-        energy = (s.double().pow(2).sum(-1) / nb)
-        worst["max_abs_err"] = max(worst["max_abs_err"], float(diff.abs().amax()))
-        worst["rel_fro_err"] = max(worst["rel_fro_err"], float(rel.max()))
-        worst["energy_retained"] = min(worst["energy_retained"], float(energy.min()))
-        if b == 0:
-            first = {"max_abs_err": round(float(diff[0].abs().amax()), 8), "rel_fro_err": round(float(rel[0]), 8),
-                     "energy_retained": round(float(energy[0]), 8)}
-        del bias, diff
-    torch.cuda.synchronize()
-    secs = time.perf_counter() - t0
-    method = "cuSOLVER SVD (fp64)" if cfg["bias"] == "af3" else "randomized SVD (fp32, cuBLAS GEMM + QR)"
-    fact = {"rank": R, "method": method, "heads": B * len(heads), "device_seconds": round(secs, 3),
-            "ours_worst_head": {k_: round(v_, 8) for k_, v_ in worst.items()}, "ours_head0": first}
-    del fb
-    return fq, fk, fact
-
-
-def reference_svd_report(cfg, n_heads: int = 1):
-    """The reference's own error on sampled heads: oracle svd_decompose (numpy
-    LAPACK dgesdd, float64; restating ref decompose.py:98-138) of the same exact
-    dense bias, next to our device factors' error on that head."""
-    import torch
-
-    from oracle import flashbias_oracle as orc
-    R, out = int(cfg["R"]), []
-    for h in range(n_heads):
-        bias = dense_biases(cfg, [h], "cuda", 0)[0]
-        b64 = bias.double().cpu().numpy()
-        t0 = time.perf_counter()
-        _, _, rep = orc.svd_decompose(b64, rank=R)
-        out.append(dict(head=h, seconds=round(time.perf_counter() - t0, 2),
-                        **{k_: round(float(v_), 8) for k_, v_ in rep.items() if k_ != "rank_used"}))
-        del bias
-    return out
-
-
 def step_fn(cfg, inp, mode: str):
     """One pass of the hot path: forward (+ backward) through the public API."""
     import paper_2505_12044_b200 as fb
