@@ -231,8 +231,10 @@ def svd_factors(cfg, heads, device):
         else:  # randomized range finder (K7), batched over the heads of this batch row
             u, s, vh = randomized_svd(bias, R)
         root = s.sqrt()
-        fq[b] = (u * root[..., None, :]).float()
-        fk[b] = (vh.transpose(-1, -2) * root[..., None, :]).float()
+        # the approximate factorisation emits bf16 factors: bf16-exact inputs need no split under
+        # the Q' = [scale*q, U] fold (their rounding is part of the reported reconstruction error)
+        fq[b] = (u * root[..., None, :]).to(torch.bfloat16).float()
+        fk[b] = (vh.transpose(-1, -2) * root[..., None, :]).to(torch.bfloat16).float()
         diff = fq[b].double() @ fk[b].double().transpose(-1, -2) - bias.double()
         nb = bias.double().pow(2).sum((-1, -2))
         rel = (diff.pow(2).sum((-1, -2)) / nb).sqrt()
@@ -247,7 +249,8 @@ def svd_factors(cfg, heads, device):
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     method = "cuSOLVER SVD (fp64)" if cfg["bias"] == "af3" else "randomized SVD (fp32, cuBLAS GEMM + QR)"
-    fact = {"rank": R, "method": method, "heads": B * len(heads), "device_seconds": round(secs, 3),
+    fact = {"rank": R, "method": method, "factor_dtype": "bf16", "heads": B * len(heads),
+            "device_seconds": round(secs, 3),
             "ours_worst_head": {k_: round(v_, 8) for k_, v_ in worst.items()}, "ours_head0": first}
     del fb
     return fq, fk, fact

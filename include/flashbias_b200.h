@@ -13,7 +13,7 @@
  *   fb_attn_fwd        flashbias_attention      attention.py:205-230
  *                      tiled_attention (Dense)  attention.py:140-202 (187-188)
  *                      tiled_attention (NoBias) attention.py:140-202
- *   fb_attn_bwd        (no reference: SPEC.md:183) — gradient of the above,
+ *   fb_attn_bwd[_ex]   (no reference: SPEC.md:183) — gradient of the above,
  *                      restated in oracle/flashbias_oracle.py:attention_bwd
  *   fb_prepare_factors concat_cols(q, sqrt(C)*fq) / concat_cols(k, fk)
  *                      core.py:54-62 called at attention.py:227-228, plus the
@@ -98,6 +98,19 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v,
                 int mask, float scale, fb_tensor* dq, fb_tensor* dk,
                 fb_tensor* dv, fb_tensor* duq, fb_tensor* duk,
                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* fb_attn_bwd with flags.  FB_BWD_DETERMINISTIC: the two-kernel backward
+ * (dK'/dV key-stationary + dQ' query-stationary, no atomics): bitwise
+ * reproducible run to run and across head shardings, at 7 GEMMs per tile
+ * instead of 5.  The default (flags = 0) accumulates dQ with fp32 L2
+ * reduce-adds whose order varies between runs. */
+#define FB_BWD_DETERMINISTIC 1
+int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v,
+                   const fb_tensor* uq, const fb_tensor* uk, const fb_tensor* bias,
+                   const fb_tensor* o, const fb_tensor* lse, const fb_tensor* dout,
+                   int mask, float scale, fb_tensor* dq, fb_tensor* dk,
+                   fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, int flags,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k);
 

@@ -24,7 +24,7 @@ MASK_CODES = {"none": 0, "causal": 1}
 
 #: every symbol the public header declares (tests check the .so exports them)
 EXPORTED_SYMBOLS = (
-    "fb_attn_fwd", "fb_attn_bwd", "fb_bwd_workspace_bytes", "fb_prepare_factors",
+    "fb_attn_fwd", "fb_attn_bwd", "fb_attn_bwd_ex", "fb_bwd_workspace_bytes", "fb_prepare_factors",
     "fb_factor_rpad", "fb_factor_cols", "fb_fold_factor_grads", "fb_factor_alibi",
     "fb_factor_spatial", "fb_dense_from_factors", "fb_bwd_preprocess", "fb_last_error",
     "fb_abi_version", "fb_launch_count", "fb_mlp_factor_panels", "fb_prepare_factor_pair",
@@ -49,6 +49,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     sig = {
         "fb_attn_fwd": (i32, [_P, _P, _P, _P, _P, _P, i32, f32, _P, _P, vp]),
         "fb_attn_bwd": (i32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, i32, f32, _P, _P, _P, _P, _P, vp, sz, vp]),
+        "fb_attn_bwd_ex": (i32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, i32, f32, _P, _P, _P, _P, _P, i32, vp, sz,
+                                 vp]),
         "fb_bwd_workspace_bytes": (sz, [_P, _P]),
         "fb_prepare_factors": (i32, [_P, i32, i32, f32, _P, vp]),
         "fb_factor_rpad": (i64, [i64, i32]),

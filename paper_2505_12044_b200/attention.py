@@ -345,7 +345,10 @@ def _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale, need_lse=True):
     return o, lse
 
 
-def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad):
+FB_BWD_DETERMINISTIC = 1
+
+
+def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad, deterministic=False):
     import torch
     lib = _lib.lib()
     D = _lib.desc
@@ -361,11 +364,12 @@ def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad)
         dq_d, k_d = D(q), D(k)
         ws_bytes = int(lib.fb_bwd_workspace_bytes(_lib.ref(dq_d), _lib.ref(k_d)))
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
-        _lib.check(lib.fb_attn_bwd(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)), _lib.ref(D(uk)),
-                                   _lib.ref(D(bias)), _lib.ref(D(o)), _lib.ref(D(lse)), _lib.ref(D(do)), mask_code,
-                                   float(scale), _lib.ref(D(dq)), _lib.ref(D(dk)), _lib.ref(D(dv)),
-                                   _lib.ref(D(duq)), _lib.ref(D(duk)), ws.data_ptr(), ws_bytes,
-                                   _lib.stream_ptr(q.device)))
+        _lib.check(lib.fb_attn_bwd_ex(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)),
+                                      _lib.ref(D(uk)), _lib.ref(D(bias)), _lib.ref(D(o)), _lib.ref(D(lse)),
+                                      _lib.ref(D(do)), mask_code, float(scale), _lib.ref(D(dq)), _lib.ref(D(dk)),
+                                      _lib.ref(D(dv)), _lib.ref(D(duq)), _lib.ref(D(duk)),
+                                      FB_BWD_DETERMINISTIC if deterministic else 0, ws.data_ptr(), ws_bytes,
+                                      _lib.stream_ptr(q.device)))
     return dq, dk, dv, duq, duk
 
 
@@ -376,30 +380,30 @@ def _make_fn():
         """Autograd wrapper: forward K1/K3, backward K2/K4 (+ factor gradients)."""
 
         @staticmethod
-        def forward(ctx, q, k, v, fq, fk, bias, mask_code, scale, premul, split):
+        def forward(ctx, q, k, v, fq, fk, bias, mask_code, scale, premul, split, deterministic=False):
             uq = uk = None
             if fq is not None:
                 uq, uk = prepare_factor_panels(fq, fk, premul, split, q.dtype)
             o, lse = _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale)
             ctx.save_for_backward(q, k, v, uq, uk, bias, o, lse, fq, fk)
-            ctx.cfg = (mask_code, scale, premul, split)
+            ctx.cfg = (mask_code, scale, premul, split, deterministic)
             return o
 
         @staticmethod
         def backward(ctx, do):
             q, k, v, uq, uk, bias, o, lse, fq, fk = ctx.saved_tensors
-            mask_code, scale, premul, split = ctx.cfg
+            mask_code, scale, premul, split, deterministic = ctx.cfg
             if bias is not None and ctx.needs_input_grad[5]:
                 raise NotImplementedError("gradient w.r.t. a dense bias is not produced (static bias)")
             want_fg = fq is not None and (ctx.needs_input_grad[3] or ctx.needs_input_grad[4])
             dq, dk, dv, duq, duk = _bwd_launch(q, k, v, uq, uk, bias, o, lse, do.contiguous(), mask_code, scale,
-                                               want_fg)
+                                               want_fg, deterministic)
             dfq = dfk = None
             if want_fg:
                 # the kernel's duq is d/d(uq) of scale*uq.uk; uq = premul*fq -> dfq = premul*duq
                 dfq = fold_factor_grads(duq, fq, 0, split, premul).to(fq.dtype)
                 dfk = fold_factor_grads(duk, fk, 1, split, 1.0).to(fk.dtype)
-            return dq, dk, dv, dfq, dfk, None, None, None, None, None
+            return dq, dk, dv, dfq, dfk, None, None, None, None, None, None
 
     return FlashBiasFunction
 
@@ -418,7 +422,8 @@ def _needs_grad(*ts) -> bool:
     return any(t is not None and _is_torch(t) and t.requires_grad for t in ts)
 
 
-def _attention(q, k, v, *, fq=None, fk=None, bias=None, mask="none", scale=None, precision=None, split=None):
+def _attention(q, k, v, *, fq=None, fk=None, bias=None, mask="none", scale=None, precision=None, split=None,
+               deterministic=False):
     """Shared driver: logits = scale*q.k + fq.fk + bias (+ causal); normalise
     inputs, run the kernel, mirror the input layout."""
     import torch
@@ -433,10 +438,11 @@ def _attention(q, k, v, *, fq=None, fk=None, bias=None, mask="none", scale=None,
     device = shp.device if (shp.device is not None and shp.device.type == "cuda") else torch.device("cuda")
     cdt = _compute_dtype(shp, precision)
     with torch.cuda.device(device):
-        return _attention_on_device(q, k, v, fq, fk, bias, mask, float(scale), cdt, split, shp, device, n, m, c)
+        return _attention_on_device(q, k, v, fq, fk, bias, mask, float(scale), cdt, split, shp, device, n, m, c,
+                                    deterministic)
 
 
-def _attention_on_device(q, k, v, fq, fk, bias, mask, scale, cdt, split, shp, device, n, m, c):
+def _attention_on_device(q, k, v, fq, fk, bias, mask, scale, cdt, split, shp, device, n, m, c, deterministic):
     import torch
     qt = _to_torch(q, "q", device, cdt)
     kt = _to_torch(k, "k", device, cdt)
@@ -496,7 +502,7 @@ def _attention_on_device(q, k, v, fq, fk, bias, mask, scale, cdt, split, shp, de
             sp, premul, kscale = plan.split, plan.premul, plan.kernel_scale
             if plan.q_fold:  # Q' = [scale*q, U]: autograd carries d/dq = scale * d/dQ'
                 qp = qp * scale
-        o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(kscale), float(premul), sp)
+        o = _fn().apply(qp, kp, vp, fqt, fkt, bp, mask_code, float(kscale), float(premul), sp, bool(deterministic))
         o = o[..., : vt.shape[-1]]
     return _mirror(o, shp)
 
@@ -520,32 +526,33 @@ def _check_tiles(tiles) -> None:
 
 # ---------------------------------------------------------------- public API
 def flashbias_attention(q, k, v, fq, fk, mask: str = MASK_NONE, tiles: Optional[TileConfig] = None, *,
-                        precision: Optional[str] = None, split: Optional[int] = None):
+                        precision: Optional[str] = None, split: Optional[int] = None, deterministic: bool = False):
     """softmax(q k^T / sqrt(C) + fq fk^T) v without materialising the bias
     (attention.py:205-230): widened contraction [q | sqrt(C) fq][k | fk]^T with
     the original 1/sqrt(C) scale, folded into the tcgen05 kernel."""
     _check_tiles(tiles)
     c = int(q.shape[-1])
     return _attention(q, k, v, fq=fq, fk=fk, mask=mask, scale=1.0 / math.sqrt(c), precision=precision,
-                      split=split)
+                      split=split, deterministic=deterministic)
 
 
 def tiled_attention(q, k, v, bias=NO_BIAS, mask: str = MASK_NONE, tiles: Optional[TileConfig] = None,
                     scale: Optional[float] = None, *, precision: Optional[str] = None,
-                    split: Optional[int] = None):
+                    split: Optional[int] = None, deterministic: bool = False):
     """Streaming attention with NoBias / DenseBias / FactoredBias (attention.py:140-202)."""
     _check_tiles(tiles)
     c = int(q.shape[-1])
     if scale is None:
         scale = 1.0 / math.sqrt(c)
     if isinstance(bias, NoBias):
-        return _attention(q, k, v, mask=mask, scale=scale, precision=precision)
+        return _attention(q, k, v, mask=mask, scale=scale, precision=precision, deterministic=deterministic)
     if isinstance(bias, DenseBias):
-        return _attention(q, k, v, bias=bias.b, mask=mask, scale=scale, precision=precision)
+        return _attention(q, k, v, bias=bias.b, mask=mask, scale=scale, precision=precision,
+                          deterministic=deterministic)
     if isinstance(bias, FactoredBias):
         # the factor term is added unscaled: logits = scale*q.k + fq.fk
         return _attention(q, k, v, fq=bias.fq, fk=bias.fk, mask=mask, scale=scale, precision=precision,
-                          split=split)
+                          split=split, deterministic=deterministic)
     raise ValidationError(f"unknown bias provider {type(bias).__name__}")
 
 

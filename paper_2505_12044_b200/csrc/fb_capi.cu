@@ -322,7 +322,17 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
                 const fb_tensor* dout, int mask, float scale, fb_tensor* dq, fb_tensor* dk,
                 fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, void* workspace,
                 size_t workspace_bytes, void* stream) {
+  return fb_attn_bwd_ex(q, k, v, uq, uk, bias, o, lse, dout, mask, scale, dq, dk, dv, duq, duk, 0, workspace,
+                        workspace_bytes, stream);
+}
+
+int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, const fb_tensor* uq,
+                   const fb_tensor* uk, const fb_tensor* bias, const fb_tensor* o, const fb_tensor* lse,
+                   const fb_tensor* dout, int mask, float scale, fb_tensor* dq, fb_tensor* dk,
+                   fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, int flags, void* workspace,
+                   size_t workspace_bytes, void* stream) {
   int rc;
+  if (flags & ~FB_BWD_DETERMINISTIC) return fail(FB_EVALUE, "unknown backward flags 0x%x", flags);
   if ((rc = check_qkv(q, k, v))) return rc;
   if ((rc = check_mask(mask, q->shape[2], k->shape[2]))) return rc;
   if ((rc = check_factors(q, k, uq, uk))) return rc;
@@ -406,8 +416,10 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     const char* v = getenv("FB_FORCE_SPLIT_BWD");
     return v && v[0] == '1' ? 1 : 0;
   }();
-  // testing hook: FB_FORCE_SPLIT_BWD=1 selects the deterministic two-kernel backward (read once, immutable)
-  const bool fused = !force_split && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
+  // FB_BWD_DETERMINISTIC (or the FB_FORCE_SPLIT_BWD=1 testing hook, read once) selects the two-kernel
+  // backward: no atomics, every gradient element written once in a fixed order
+  const bool deterministic = force_split || (flags & FB_BWD_DETERMINISTIC);
+  const bool fused = !deterministic && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
   if (fused) {
     float* acc = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(delta) +
                                           ((size_t)B * H * N * sizeof(float) + 255) / 256 * 256);

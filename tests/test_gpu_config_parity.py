@@ -166,3 +166,31 @@ def test_dense_bias_masking_trailing_key_blocks_is_finite():
         _check_head({"o": _np(o[0, h]), "dq": _np(dq[0, h]), "dk": _np(dk[0, h]), "dv": _np(dv[0, h])}, ref,
                     ("o", "dq", "dk", "dv"), f"masked dense head {h}")
     assert float(dk[..., 300:, :].abs().max()) == 0.0 and float(dv[..., 300:, :].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("D,R", [(128, 2), (64, 9)])
+def test_deterministic_backward_is_bitwise_and_shard_invariant(D, R):
+    """deterministic=True (FB_BWD_DETERMINISTIC, the two-kernel backward): two
+    runs are bitwise equal, and computing 4 heads in one call equals computing
+    them as two 2-head shards (SURVEY §8(e)'s G=1 vs G=2 invariance)."""
+    N, H = 640, 4
+    q, k, v, do = (_rand((1, H, N, D), 300 + i) for i in range(4))
+    g = torch.Generator(device="cuda").manual_seed(9)
+    fq = (torch.randn(1, H, N, R, generator=g, device="cuda") * 0.3).contiguous()
+    fk = (torch.randn(1, H, N, R, generator=g, device="cuda") * 0.3).contiguous()
+
+    def grads(lo, hi):
+        qq, kk, vv = (t[:, lo:hi].detach().clone().requires_grad_(True) for t in (q, k, v))
+        o = fb.flashbias_attention(qq, kk, vv, fq[:, lo:hi], fk[:, lo:hi], mask="causal", deterministic=True)
+        return [o.detach()] + list(torch.autograd.grad(o, (qq, kk, vv), do[:, lo:hi]))
+
+    a, b = grads(0, H), grads(0, H)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    s0, s1 = grads(0, 2), grads(2, H)
+    for x, y0, y1 in zip(a, s0, s1):
+        assert torch.equal(x, torch.cat([y0, y1], 1))
+    ref = orc.attention_bwd(_np(q[0, 0]), _np(k[0, 0]), _np(v[0, 0]), _np(do[0, 0]), fq=_np(fq[0, 0]),
+                            fk=_np(fk[0, 0]), premul=math.sqrt(D), mask="causal")
+    _check_head({"o": _np(a[0][0, 0]), "dq": _np(a[1][0, 0]), "dk": _np(a[2][0, 0]), "dv": _np(a[3][0, 0])}, ref,
+                ("o", "dq", "dk", "dv"), "deterministic head 0")
