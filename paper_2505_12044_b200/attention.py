@@ -244,14 +244,28 @@ def choose_split(fq, fk, premul: float = 1.0, tol: float = 1e-2, max_cols: int =
     return k
 
 
-def plan_factor_fold(fq, fk, scale: float, tol: float = 1e-2, max_cols: int = 64, panel_dtype=None) -> FactorPlan:
+def plan_factor_fold(fq, fk, scale: float, tol: float = 1e-2, max_cols: int = 64, panel_dtype=None,
+                     shard_invariant: bool = False) -> FactorPlan:
     """Pick the fold and split for logits = scale*q.k + fq.fk (see FactorPlan).
 
     The reference order is kept whenever 1/scale is a power of two (exact) or
     it needs no more columns; otherwise Q' = [scale*q, U] avoids the
-    premultiplier's rounding.  Raises ConfigError if neither meets ``tol``."""
+    premultiplier's rounding.  Raises ConfigError if neither meets ``tol``.
+
+    ``shard_invariant``: the split level must not depend on WHICH heads share
+    the launch (the bound is a max over them), so use the most accurate level
+    that fits ``max_cols`` -- a function of R alone -- and only check ``tol``."""
     pm = 1.0 / scale
     r = int(fq.shape[-1])
+    if shard_invariant:
+        kfit = max([k for k in (1, 2, 3) if r * k * (k + 1) // 2 <= max_cols] or [0])
+        if kfit:
+            ba, bq = _split_bounds(fq, fk, [pm, 1.0], panel_dtype)
+            if ba[kfit - 1] * scale <= tol:
+                return FactorPlan(kfit, False, pm, scale)
+            if bq[kfit - 1] <= tol:
+                return FactorPlan(kfit, True, 1.0, 1.0)
+        raise ConfigError(f"rank-{r} factors cannot meet {tol:g} logits within {max_cols} panel columns")
     if _is_pow2(pm):
         ba = _split_bounds(fq, fk, [pm], panel_dtype)[0]
         ka, kq, bq = _split_level(ba, scale, r, tol, max_cols), None, None
@@ -274,7 +288,7 @@ def _base_of(t):
 
 
 def plan_factor_fold_cached(fq_user, fk_user, fq, fk, scale: float, tol: float = 1e-2,
-                            max_cols: int = 64, panel_dtype=None) -> FactorPlan:
+                            max_cols: int = 64, panel_dtype=None, shard_invariant: bool = False) -> FactorPlan:
     """plan_factor_fold memoised per user factor tensors (the decision needs a
     device->host read; static factors such as ALiBi/spatial pay it once).
 
@@ -285,16 +299,17 @@ def plan_factor_fold_cached(fq_user, fk_user, fq, fk, scale: float, tol: float =
     inputs (a fresh device copy every call) are not cached."""
     import weakref
     if not (_is_torch(fq_user) and _is_torch(fk_user)):
-        return plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype)
+        return plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype, shard_invariant)
     bq, bk = _base_of(fq_user), _base_of(fk_user)
 
     def geom(t, base):
         return (id(base), base._version, t.storage_offset(), tuple(t.shape), tuple(t.stride()), t.dtype)
-    key = (geom(fq_user, bq), geom(fk_user, bk), float(scale), float(tol), int(max_cols), str(panel_dtype))
+    key = (geom(fq_user, bq), geom(fk_user, bk), float(scale), float(tol), int(max_cols), str(panel_dtype),
+           bool(shard_invariant))
     hit = _SPLIT_CACHE.get(key)
     if hit is not None and hit[0]() is bq and hit[1]() is bk:
         return hit[2]
-    plan = plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype)
+    plan = plan_factor_fold(fq, fk, scale, tol, max_cols, panel_dtype, shard_invariant)
     if len(_SPLIT_CACHE) > 256:
         _SPLIT_CACHE.clear()
     _SPLIT_CACHE[key] = (weakref.ref(bq), weakref.ref(bk), plan)
@@ -498,7 +513,8 @@ def _attention_on_device(q, k, v, fq, fk, bias, mask, scale, cdt, split, shp, de
             if split is not None:
                 plan = FactorPlan(int(split), False, 1.0 / scale, scale)
             else:
-                plan = plan_factor_fold_cached(fq, fk, fqt, fkt, scale, max_cols=max_cols, panel_dtype=cdt)
+                plan = plan_factor_fold_cached(fq, fk, fqt, fkt, scale, max_cols=max_cols, panel_dtype=cdt,
+                                               shard_invariant=deterministic)
             sp, premul, kscale = plan.split, plan.premul, plan.kernel_scale
             if plan.q_fold:  # Q' = [scale*q, U]: autograd carries d/dq = scale * d/dQ'
                 qp = qp * scale
@@ -529,7 +545,11 @@ def flashbias_attention(q, k, v, fq, fk, mask: str = MASK_NONE, tiles: Optional[
                         precision: Optional[str] = None, split: Optional[int] = None, deterministic: bool = False):
     """softmax(q k^T / sqrt(C) + fq fk^T) v without materialising the bias
     (attention.py:205-230): widened contraction [q | sqrt(C) fq][k | fk]^T with
-    the original 1/sqrt(C) scale, folded into the tcgen05 kernel."""
+    the original 1/sqrt(C) scale, folded into the tcgen05 kernel.
+
+    ``deterministic``: bitwise-reproducible gradients (two-kernel backward, no
+    atomics) and a factor split level that depends on the rank only, so the
+    result of a head does not depend on the heads it is launched with."""
     _check_tiles(tiles)
     c = int(q.shape[-1])
     return _attention(q, k, v, fq=fq, fk=fk, mask=mask, scale=1.0 / math.sqrt(c), precision=precision,
