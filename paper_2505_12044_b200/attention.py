@@ -334,6 +334,30 @@ def prepare_factor_panels(fq, fk, premul: float, split: int, dtype):
     return uq, uk
 
 
+_PANEL_CACHE: dict = {}
+
+
+def prepare_factor_panels_cached(fq, fk, premul: float, split: int, dtype):
+    """prepare_factor_panels memoised on the factor tensors' identity (base
+    object by weak reference + view geometry + in-place version counter), so
+    static factors (ALiBi, spatial, offline SVD) are split into panels once,
+    not every step; any in-place update (an optimizer step) re-splits."""
+    import weakref
+    bq, bk = _base_of(fq), _base_of(fk)
+
+    def geom(t, base):
+        return (id(base), base._version, t.storage_offset(), tuple(t.shape), tuple(t.stride()), t.dtype, t.device)
+    key = (geom(fq, bq), geom(fk, bk), float(premul), int(split), dtype)
+    hit = _PANEL_CACHE.get(key)
+    if hit is not None and hit[0]() is bq and hit[1]() is bk:
+        return hit[2]
+    panels = prepare_factor_panels(fq, fk, premul, split, dtype)
+    if len(_PANEL_CACHE) >= 8:
+        _PANEL_CACHE.pop(next(iter(_PANEL_CACHE)))
+    _PANEL_CACHE[key] = (weakref.ref(bq), weakref.ref(bk), panels)
+    return panels
+
+
 def fold_factor_grads(dpanel, like, side: int, split: int, postmul: float):
     """fb_fold_factor_grads: split-panel gradients -> logical factor gradient shaped like ``like``."""
     import torch
@@ -398,7 +422,7 @@ def _make_fn():
         def forward(ctx, q, k, v, fq, fk, bias, mask_code, scale, premul, split, deterministic=False):
             uq = uk = None
             if fq is not None:
-                uq, uk = prepare_factor_panels(fq, fk, premul, split, q.dtype)
+                uq, uk = prepare_factor_panels_cached(fq, fk, premul, split, q.dtype)
             o, lse = _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale)
             ctx.save_for_backward(q, k, v, uq, uk, bias, o, lse, fq, fk)
             ctx.cfg = (mask_code, scale, premul, split, deterministic)

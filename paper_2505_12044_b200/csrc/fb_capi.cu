@@ -430,8 +430,6 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
     tacc.dtype = FB_F32;
     CUtensorMap macc;
     if ((rc = make_map(&macc, &tacc, D, 32, 0, "dq_acc"))) return rc;
-    e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * D * sizeof(float), s);
-    if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
     static const int t128_off = [] {
       const char* v = getenv("FB_BWD_T128");
       return v && v[0] == '0' ? 1 : 0;
@@ -455,7 +453,11 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
       e = launch_dq_convert_t(acc, (int)n4, p, q->dtype == FB_BF16, s);
       note_launch(2);
       return e == cudaSuccess ? FB_OK : cuda_fail(e, "dq_convert_t");
-    } else if (D == 128) {
+    }
+    // the 64-query kernels reduce into the untransposed [B,H,N,D] accumulator: start from zero
+    e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * D * sizeof(float), s);
+    if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
+    if (D == 128) {
       e = launch_bwd_fused_sm100(rp, bias != nullptr, q->dtype == FB_BF16, maps, macc, p, s);
     } else {
       CUtensorMap mduq;
