@@ -27,6 +27,18 @@
 // [0,64) / [64,128) (thread = key row = TMEM lane), 8-11 dQ drain (thread =
 // head-dim lane of dQ^T: TMEM -> smem -> TMA reduce-add into the fp32 dQ
 // accumulator), warp 12 TMA producer, warp 13 TMEM alloc + MMA issuer.
+//
+// MC (cluster multicast) variant: a cluster of two CTAs owns two adjacent key
+// tiles of one head and streams the SAME query blocks in lockstep, so each
+// Q / dO / Uq tile is read from L2 once for both SMs: each CTA's producer
+// loads one 64-column atom and multicasts it to both CTAs (the full barriers
+// expect the whole tile), and a slot is refilled only after BOTH CTAs' MMAs
+// have released it (multicast commits, empty barriers count 2).  L2 is the
+// shared bottleneck of this kernel (the dQ reduce-adds and these loads go
+// through the same slices: tests/gpu_probe/reduce_rate.cu), so halving the
+// load traffic leaves more of it to the reductions.  Causal: both CTAs start
+// at the even tile's diagonal block; for the odd tile that first block is
+// fully masked (P = dS = 0) and its dQ reduction is skipped.
 #include "fb_kernels.h"
 #include "fb_sm100.cuh"
 
@@ -97,7 +109,7 @@ struct T128Bars {
   uint32_t tmem_base;
 };
 
-template <int RP, bool BF16>
+template <int RP, bool BF16, bool MC>
 __global__ void __launch_bounds__(512, 1)
     fb_bwd_t128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_uq, const __grid_constant__ CUtensorMap tm_k,
@@ -121,8 +133,11 @@ __global__ void __launch_bounds__(512, 1)
   const int h = bh / p.B, b = bh % p.B;
   const int kv0 = kt * 128;
   const int nqb = (p.N + 127) / 128;
-  const int i_start = p.causal ? kt : 0;
+  // MC: the pair (even tile, odd tile) shares one query-block stream starting at the even tile's diagonal
+  const uint32_t crank = MC ? cluster_ctarank() : 0u;
+  const int i_start = p.causal ? (MC ? (kt & ~1) : kt) : 0;
   const int nblk = nqb > i_start ? nqb - i_start : 0;
+  constexpr uint16_t kPair = 3;
 
   if (warp == 12 && lane == 0) {
     tma_prefetch(&tm_q);
@@ -137,10 +152,10 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(&bars->res_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars->q_full[i], 1);
-      mbar_init(&bars->q_empty[i], 1);
+      mbar_init(&bars->q_empty[i], MC ? 2 : 1);  // MC: released by both CTAs' MMAs
     }
     mbar_init(&bars->do_full, 1);
-    mbar_init(&bars->do_empty, 1);
+    mbar_init(&bars->do_empty, MC ? 2 : 1);
     mbar_init(&bars->s_full, 1);
     mbar_init(&bars->p_ready, 8);
     mbar_init(&bars->dp_full, 1);
@@ -154,6 +169,7 @@ __global__ void __launch_bounds__(512, 1)
   if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync_all();  // both CTAs' barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
   constexpr uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 384;
@@ -177,14 +193,26 @@ __global__ void __launch_bounds__(512, 1)
         if (use > 0) mbar_wait(&bars->q_empty[slot], (use - 1) & 1);
         uint8_t* qd = smem + Cfg::kQ0 + slot * Cfg::kQSlot;
         mbar_arrive_expect_tx(&bars->q_full[slot], Cfg::kTile + RP * Cfg::kPanel);
-        for (int a = 0; a < 2; ++a) tma_load_4d(qd + a * 16384, &tm_q, &bars->q_full[slot], a * 64, q0, h, b);
-        for (int pn = 0; pn < RP; ++pn)
-          tma_load_4d(qd + Cfg::kTile + pn * Cfg::kPanel, &tm_uq, &bars->q_full[slot], pn * 16, q0, hq, bq);
+        if constexpr (MC) {  // this CTA's atom (and CTA 0: the factor panels) to both CTAs
+          tma_load_4d_mc(qd + crank * 16384, &tm_q, &bars->q_full[slot], crank * 64, q0, h, b, kPair);
+          if (crank == 0)
+            for (int pn = 0; pn < RP; ++pn)
+              tma_load_4d_mc(qd + Cfg::kTile + pn * Cfg::kPanel, &tm_uq, &bars->q_full[slot], pn * 16, q0, hq, bq,
+                             kPair);
+        } else {
+          for (int a = 0; a < 2; ++a) tma_load_4d(qd + a * 16384, &tm_q, &bars->q_full[slot], a * 64, q0, h, b);
+          for (int pn = 0; pn < RP; ++pn)
+            tma_load_4d(qd + Cfg::kTile + pn * Cfg::kPanel, &tm_uq, &bars->q_full[slot], pn * 16, q0, hq, bq);
+        }
         if (j > 0) mbar_wait(&bars->do_empty, (j - 1) & 1);
         trace(p.trace, p.trace_cta, 21, j);
         mbar_arrive_expect_tx(&bars->do_full, Cfg::kTile);
-        for (int a = 0; a < 2; ++a)
-          tma_load_4d(smem + Cfg::kDO + a * 16384, &tm_do, &bars->do_full, a * 64, q0, h, b);
+        if constexpr (MC) {
+          tma_load_4d_mc(smem + Cfg::kDO + crank * 16384, &tm_do, &bars->do_full, crank * 64, q0, h, b, kPair);
+        } else {
+          for (int a = 0; a < 2; ++a)
+            tma_load_4d(smem + Cfg::kDO + a * 16384, &tm_do, &bars->do_full, a * 64, q0, h, b);
+        }
       }
     } else if (warp == 13 && lane == 0 && nblk > 0) {
       // ------------------------------------------------------------ MMA issuer
@@ -235,7 +263,8 @@ __global__ void __launch_bounds__(512, 1)
         for (int kk = 0; kk < 8; ++kk)  // K = 128 queries; P^T of group g sits at columns [64g, 64g+32)
           mma_ts(tmem + T_DV, tmem + T_S + (kk >> 2) * 64 + (kk & 3) * 8, dm_do + kk * kRow16, id_d,
                  (j > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&bars->do_empty);
+        if constexpr (MC) tc_commit_mc(&bars->do_empty, kPair);
+        else tc_commit(&bars->do_empty);
       };
       auto issue_dqk = [&](int j) {
         mbar_wait(&bars->ds_ready, j & 1);
@@ -251,7 +280,8 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dK += dS^T Q (K = 128 queries)
           mma_ss(tmem + T_DK, dk_ds + ks(kk), dm_q + kk * kRow16, id_d, (j > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(&bars->q_empty[j & 1]);
+        if constexpr (MC) tc_commit_mc(&bars->q_empty[j & 1], kPair);
+        else tc_commit(&bars->q_empty[j & 1]);
         tc_commit(&bars->ds_free);
       };
       mbar_wait(&bars->res_full, 0);
@@ -311,7 +341,7 @@ __global__ void __launch_bounds__(512, 1)
           pr[c + 1] = x.y;
         }
       }
-      if (p.causal && j == 0) {  // diagonal block: key kv sees queries q >= kv
+      if (p.causal && q0 <= kv0) {  // diagonal block (MC odd tile: also the fully masked block before it)
         const int qb = q0 + 64 * g;
 #pragma unroll
         for (int c = 0; c < 64; ++c)
@@ -430,10 +460,14 @@ __global__ void __launch_bounds__(512, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->dq_free);
       constexpr int QC = T128_QCHUNK, RB = QC * 4, NST = 16384 / (128 * RB);  // row bytes, stages
+      // MC odd tile, causal: the first shared block lies entirely above this tile's diagonal (dQ^T = 0)
+      const bool skip = MC && p.causal && q0 + 128 <= kv0;
 #pragma unroll
-      for (int c = 0; c < 128 / QC; ++c, ++chunk) {
+      for (int c = 0; c < (skip ? 0 : 128 / QC); ++c, ++chunk) {
         uint8_t* stg = reinterpret_cast<uint8_t*>(dq_stage) + (chunk % NST) * (128 * RB);
+        if (leader) trace(p.trace, p.trace_cta, 26, j * 8 + c);
         if (leader) t128_wait_read<NST - 1>();  // the reduction that last read this stage has finished reading
+        if (leader) trace(p.trace, p.trace_cta, 27, j * 8 + c);
         named_bar_sync(3, 128);
         const float sc = p.scale;
 #pragma unroll
@@ -443,9 +477,12 @@ __global__ void __launch_bounds__(512, 1)
               make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
                           __uint_as_float(v[e + 3]) * sc);
         }
+        if (leader) trace(p.trace, p.trace_cta, 28, j * 8 + c);
         fence_proxy_async();
+        if (leader) trace(p.trace, p.trace_cta, 29, j * 8 + c);
         named_bar_sync(3, 128);
         if (leader) {
+          trace(p.trace, p.trace_cta, 30, j * 8 + c);
           t128_reduce_add(&tm_dqacc, stg, q0 + QC * c, 0, h, b);
           t128_bulk_commit();
         }
@@ -457,22 +494,47 @@ __global__ void __launch_bounds__(512, 1)
 
   tc_fence_before();
   __syncthreads();
+  // MC: the peer's last multicast commits / loads target this CTA's smem: exit together
+  if constexpr (MC) cluster_sync_all();
   if (warp == 13) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
 }
 
-template <int RP, bool BF16>
-static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, const BwdParams& p, cudaStream_t s) {
+#ifndef T128_MULTICAST
+#define T128_MULTICAST 1
+#endif
+
+template <int RP, bool BF16, bool MC>
+static cudaError_t launch_t128_mc(const BwdMaps& m, const CUtensorMap& dqacc, const BwdParams& p, cudaStream_t s) {
   using Cfg = T128Cfg<RP>;
-  auto k = fb_bwd_t128_kernel<RP, BF16>;
+  auto k = fb_bwd_t128_kernel<RP, BF16, MC>;
   static std::atomic<uint64_t> attr_mask{0};
   cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(k), Cfg::kSmem);
   if (e != cudaSuccess) return e;
-  k<<<((p.M + 127) / 128) * p.B * p.H, 512, Cfg::kSmem, s>>>(m.q128, m.do128, m.uq128, m.k128, m.v128, m.uk128,
-                                                            dqacc, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(((p.M + 127) / 128) * p.B * p.H);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = MC ? 2 : 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k, m.q128, m.do128, m.uq128, m.k128, m.v128, m.uk128, dqacc, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+// cluster pairs need an even number of key tiles per head (adjacent tiles of one head)
+template <int RP, bool BF16>
+static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, const BwdParams& p, cudaStream_t s) {
+  const int nkt = (p.M + 127) / 128;
+  if (T128_MULTICAST && nkt % 2 == 0) return launch_t128_mc<RP, BF16, true>(m, dqacc, p, s);
+  return launch_t128_mc<RP, BF16, false>(m, dqacc, p, s);
 }
 
 // dq[b,h,n,:] = acc_t[b,h,:,n]: 64-query x 128-dim tiles transposed through

@@ -35,8 +35,8 @@ names = {10: "mma dV", 11: "mma S", 12: "mma dK", 13: "mma dQ", 14: "mma dP", 15
 print(f"span {tl[-1][0]} cycles, {len(tl)} events")
 prev = None
 for t, e, i in tl:
-    if j0 <= i < j0 + nb:
-        print(f"{t:9d} {'+%d' % (t - prev) if prev is not None else '':>7s} {names.get(e, e):12s} {i}")
+    if j0 <= i < j0 + nb and e < 26:
+        print(f"{t:9d} {'+%d' % (t - prev) if prev is not None else '':>7s} {str(names.get(e, e)):12s} {i}")
         prev = t
 per = collections.defaultdict(dict)
 for t, e, i in tl:
@@ -47,3 +47,12 @@ def avg(e0, e1):
 print("A0 %.0f  A1 %.0f  B0 %.0f  B1 %.0f  drain %.0f" % (avg(15, 16), avg(22, 23), avg(17, 18), avg(24, 25), avg(19, 20)))
 s = sorted(per[11].values())
 print("period (S issue) %.1f cycles over %d blocks" % ((s[-1] - s[0]) / max(1, len(s) - 1), len(s)))
+
+# per-chunk drain breakdown (events 26..30 of the leader drain thread, index j*8+c)
+import statistics as _st
+def seg(e0, e1):
+    xs = [per[e1][i] - per[e0][i] for i in per.get(e0, {}) if i in per.get(e1, {})]
+    return _st.median(xs) if xs else float("nan")
+print("drain chunk medians: wait_read %.0f  bar1+sts %.0f  fence %.0f  bar2 %.0f  issue->next %.0f" % (
+    seg(26, 27), seg(27, 28), seg(28, 29), seg(29, 30),
+    _st.median([per[26][i + 1] - per[30][i] for i in per.get(30, {}) if i + 1 in per.get(26, {})] or [float("nan")])))
