@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import torch
 import paper_2505_12044_b200 as fb
 from paper_2505_12044_b200 import _lib
-_lib.LIB_PATH = os.path.join(os.path.dirname(_lib.LIB_PATH), "libflashbias_b200_trace.so")  # debug build
+_lib.LIB_PATH = os.path.join(os.path.dirname(_lib.LIB_PATH), os.environ.get("TRACE_LIB", "libflashbias_b200_trace.so"))  # debug build
 lib = _lib.lib()
 lib.fb_debug_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_int]
 cta = int(sys.argv[1]) if len(sys.argv) > 1 else 40
