@@ -538,6 +538,10 @@ def run_gpu(args, cfg):
                    "bwd": cfg["bwd"], "parallelism": f"bh-shard{world}",
                    "l2": ("L2 flushed (256 MB write) before every timed step, outside its events" if flush
                           else "inputs larger than L2 (no flush needed)")},
+        "collective": None if dist is None else {
+            "backend": dist.get_backend(), "nranks": world,
+            "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if dist.get_backend() == "nccl" else None,
+            "where": "after the kernels only: all-gather of O / dQ / dK / dV head slices (no data-path collective)"},
         "gather_ms_per_step": None if gather_ms is None else round(gather_ms, 3),
         "ms_per_step_with_gather": None if gather_ms is None else round(ms + gather_ms, 3),
         "dense_bias_ms_per_step": None if dense_ms is None else round(dense_ms, 3),

@@ -51,6 +51,16 @@ def _worker(rank, world, port, result_path):
     lo, hi = head_range(H, world, rank)
     part = torch.full((B, hi - lo, 2), float(rank))
     allp = gather_heads(part, H)
+    # gradients shard the same way: every rank computes dq/dk/dv/dfq/dfk of its own heads
+    do = torch.randn(B, H, N, d, generator=g, dtype=torch.float64)
+
+    def grads(qs, ks, vs, dos, fqs, fks):
+        r = orc.attention_bwd(qs.numpy(), ks.numpy(), vs.numpy(), dos.numpy(), fq=fqs.numpy(), fk=fks.numpy(),
+                              premul=np.sqrt(d), mask="causal")
+        return torch.from_numpy(np.stack([r["dq"], r["dk"], r["dv"]], 2))  # [B, H, 3, N, d]
+
+    gfull = sharded_apply(grads, [q, k, v, do, fq, fk], H)
+    gref = grads(q, k, v, do, fq, fk)
     # chunked compute + gather (slices land in place by per-rank broadcasts) == unchunked
     chunked = sharded_apply(hot, [q, k, v, fq, fk], H, chunks=2)
     # a 2-D [N, R] factor with R == H is shared, never split by columns
@@ -64,6 +74,7 @@ def _worker(rank, world, port, result_path):
         res["chunked_eq"] = bool(torch.equal(chunked, full))
         res["shared_eq"] = bool(torch.equal(got2d, q.sum(-1, keepdim=True) + shared.sum()))
         res["one_eq"] = bool(torch.equal(one, q[:, :1] * 2))
+        res["grads_eq"] = bool(torch.equal(gfull, gref))
         torch.save(res, result_path)
     dist.barrier()
     dist.destroy_process_group()
@@ -75,4 +86,4 @@ def test_sharded_equals_unsharded_gloo(tmp_path):
     res = torch.load(path)
     assert res["eq"] and res["shape"] == (2, 5, 40, 8)
     assert res["ragged"] == [0.0, 0.0, 0.0, 1.0, 1.0]
-    assert res["chunked_eq"] and res["shared_eq"] and res["one_eq"]
+    assert res["chunked_eq"] and res["shared_eq"] and res["one_eq"] and res["grads_eq"]
