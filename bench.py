@@ -527,6 +527,14 @@ def run_gpu(args, cfg):
             "factor_split": kb["split"], "factor_rpad": kb["rpad"], "q_fold": kb["q_fold"],
         }
 
+    if kb is None:  # C1: the fp32 SIMT forward is the whole step (one launch per step)
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12  # FFMA lanes x 2 flops x max SM clock
+        roofline = {"bound": "fp32 FMA (SIMT, accurate fp32 products for the 1e-5 contract)",
+                    "kernel": "fwd_simt_tiled (split-KV thread-block cluster, DSMEM combine)",
+                    "achieved": round(tflops, 2), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
+                    "frac": round(tflops / fp32_peak, 4),
+                    "peak_kind": "nominal fp32 FFMA peak (148 SMs x 128 lanes x 2 x 1965 MHz); no measured fp32 peak",
+                    "traffic": None}
     e2e = run_e2e(cfg, inp, args, device, dist=dist, total_bh=total_bh) if not args.skip_e2e else None
     result = {
         "metric": METRIC, "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,

@@ -537,32 +537,49 @@ __global__ void __launch_bounds__(128) fwd_simt_f32_kernel(const SimtParams p) {
 
 // Register-tiled SIMT forward (same numerics as fwd_simt_f32_kernel: fp32 FMA
 // q.k, fp64 factor / bias terms and running max, expf of the fp32 difference):
-// CTA = 64 query rows x 256 threads (16 x 16), KV blocks of 64 keys; thread
-// (ty, tx) owns rows 4ty..4ty+3 x keys 4tx..4tx+3 of S and rows 4ty.. x head
+// CTA = BM query rows x 256 threads (16 x 16), KV blocks of 64 keys; thread
+// (ty, tx) owns rows RT*ty.. x keys 4tx..4tx+3 of S and rows RT*ty.. x head
 // columns CPT*tx.. of O.  Q^T / K^T tiles are stored channel-major in shared
-// memory so every channel step is two float4 loads feeding 16 FMAs; P goes
+// memory so every channel step is two vector loads feeding 4*RT FMAs; P goes
 // through shared memory to the P.V product.
-template <int D, int BM>
+//
+// Split-KV over a thread-block cluster (SPLIT CTAs, one per KV range of the
+// same row block): small grids (C1: 8 heads x 1024 rows) otherwise leave most
+// SMs idle while each CTA walks every KV block serially.  Each CTA keeps its
+// partial (m, l, acc) in shared memory; after a cluster barrier the rank-0 CTA
+// reads the peers' partials over DSMEM and combines them -- no global scratch,
+// one launch.
+template <int D, int BM, int SPLIT>
 __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p) {
   constexpr int BN = 64, CPT = D / 16, RT = BM / 16;  // rows per thread
   extern __shared__ float sm[];
-  const int DK = D + p.R;
+  const int R = p.R, DK = D + R;
   float* sQ = sm;                  // [DK][BM]
   float* sK = sQ + DK * BM;        // [DK][BN]
   float* sV = sK + DK * BN;        // [BN][D]
   float* sP = sV + BN * D;         // [BM][BN + 4]
   constexpr int PST = BN + 4;
   const int b = blockIdx.z, h = blockIdx.y;
-  const int q0 = blockIdx.x * BM;
+  const int rank = SPLIT > 1 ? static_cast<int>(blockIdx.x % SPLIT) : 0;
+  const int q0 = (blockIdx.x / SPLIT) * BM;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  for (int idx = t; idx < BM * DK; idx += 256) {
-    const int r = idx / DK, c = idx % DK, row = q0 + r;
-    float v = 0.f;
-    if (row < p.N) {
-      if (c < D) v = p.q[b * p.q_sb + h * p.q_sh + static_cast<int64_t>(row) * p.q_sn + c];
-      else v = p.uq[b * p.uq_sb + h * p.uq_sh + static_cast<int64_t>(row) * p.uq_sn + (c - D)];
-    }
-    sQ[c * BM + r] = v;
+  const float* qb = p.q + b * p.q_sb + h * p.q_sh;
+  const float* kb = p.k + b * p.k_sb + h * p.k_sh;
+  const float* vb = p.v + b * p.v_sb + h * p.v_sh;
+  // q rows: D / 4 float4 per row (compile-time index math), then the R factor columns
+  for (int idx = t; idx < BM * (D / 4); idx += 256) {
+    const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4, row = q0 + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (row < p.N) v = *reinterpret_cast<const float4*>(qb + static_cast<int64_t>(row) * p.q_sn + c4);
+    sQ[(c4 + 0) * BM + r] = v.x;
+    sQ[(c4 + 1) * BM + r] = v.y;
+    sQ[(c4 + 2) * BM + r] = v.z;
+    sQ[(c4 + 3) * BM + r] = v.w;
+  }
+  for (int idx = t; idx < BM * R; idx += 256) {
+    const int r = idx / R, c = idx % R, row = q0 + r;
+    sQ[(D + c) * BM + r] =
+        row < p.N ? p.uq[b * p.uq_sb + h * p.uq_sh + static_cast<int64_t>(row) * p.uq_sn + c] : 0.f;
   }
   double m_run[RT];
   float l_run[RT], acc[RT][CPT];
@@ -573,21 +590,28 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[i][c] = 0.f;
   }
-  const int kv_end = p.causal ? min(p.M, q0 + BM) : p.M;
-  for (int kv0 = 0; kv0 < kv_end; kv0 += BN) {
+  const int kv_all = p.causal ? min(p.M, q0 + BM) : p.M;
+  const int nkv = (kv_all + BN - 1) / BN;
+  const int kb0 = nkv * rank / SPLIT, kb1 = nkv * (rank + 1) / SPLIT;  // this CTA's KV blocks
+  for (int kblk = kb0; kblk < kb1; ++kblk) {
+    const int kv0 = kblk * BN;
     __syncthreads();  // previous block's sK / sV / sP fully consumed
-    for (int idx = t; idx < BN * DK; idx += 256) {
-      const int r = idx / DK, c = idx % DK, j = kv0 + r;
-      float v = 0.f;
+    for (int idx = t; idx < BN * (D / 4); idx += 256) {
+      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4, j = kv0 + r;
+      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f), vv = kv;
       if (j < p.M) {
-        if (c < D) v = p.k[b * p.k_sb + h * p.k_sh + static_cast<int64_t>(j) * p.k_sn + c];
-        else v = p.uk[b * p.uk_sb + h * p.uk_sh + static_cast<int64_t>(j) * p.uk_sn + (c - D)];
+        kv = *reinterpret_cast<const float4*>(kb + static_cast<int64_t>(j) * p.k_sn + c4);
+        vv = *reinterpret_cast<const float4*>(vb + static_cast<int64_t>(j) * p.v_sn + c4);
       }
-      sK[c * BN + r] = v;
+      sK[(c4 + 0) * BN + r] = kv.x;
+      sK[(c4 + 1) * BN + r] = kv.y;
+      sK[(c4 + 2) * BN + r] = kv.z;
+      sK[(c4 + 3) * BN + r] = kv.w;
+      *reinterpret_cast<float4*>(sV + r * D + c4) = vv;
     }
-    for (int idx = t; idx < BN * D; idx += 256) {
-      const int r = idx / D, c = idx % D, j = kv0 + r;
-      sV[idx] = j < p.M ? p.v[b * p.v_sb + h * p.v_sh + static_cast<int64_t>(j) * p.v_sn + c] : 0.f;
+    for (int idx = t; idx < BN * R; idx += 256) {
+      const int r = idx / R, c = idx % R, j = kv0 + r;
+      sK[(D + c) * BN + r] = j < p.M ? p.uk[b * p.uk_sb + h * p.uk_sh + static_cast<int64_t>(j) * p.uk_sn + c] : 0.f;
     }
     __syncthreads();
     float s[RT][4];
@@ -687,6 +711,70 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
         for (int c = 0; c < CPT; ++c) acc[i][c] = fmaf(pv[i], vv[c], acc[i][c]);
     }
   }
+  if constexpr (SPLIT > 1) {
+    // partials -> this CTA's smem (the K/V region is free): per row m (double), l, then acc[D]
+    __syncthreads();
+    double* pm = reinterpret_cast<double*>(sK);           // [BM]
+    float* pl = reinterpret_cast<float*>(pm + BM);         // [BM]
+    float* pa = pl + BM;                                   // [BM][D]
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      const int r = RT * ty + i;
+      if (tx == 0) {
+        pm[r] = m_run[i];
+        pl[r] = l_run[i];
+      }
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) pa[r * D + CPT * tx + c] = acc[i][c];
+    }
+    cluster_sync_all();  // every rank's partial is written (release / acquire at cluster scope)
+    if (rank == 0) {
+      const uint32_t base = smem_u32(sK);
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int r = RT * ty + i;
+        double m_all = -INFINITY;
+        double mr[SPLIT];
+        float lr[SPLIT];
+#pragma unroll
+        for (int k = 0; k < SPLIT; ++k) {
+          uint32_t ra;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(k));
+          asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(mr[k]) : "r"(ra + 8u * r));
+          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lr[k]) : "r"(ra + 8u * BM + 4u * r));
+          m_all = fmax(m_all, mr[k]);
+        }
+        float wsum = 0.f, w[SPLIT];
+#pragma unroll
+        for (int k = 0; k < SPLIT; ++k) {
+          w[k] = mr[k] == -INFINITY ? 0.f : expf(static_cast<float>(mr[k] - m_all));
+          wsum += w[k] * lr[k];
+        }
+        float o[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) o[c] = 0.f;
+#pragma unroll
+        for (int k = 0; k < SPLIT; ++k) {
+          uint32_t ra;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(k));
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            float x;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];"
+                         : "=f"(x)
+                         : "r"(ra + 12u * BM + 4u * (r * D + CPT * tx + c)));
+            o[c] = fmaf(w[k], x, o[c]);
+          }
+        }
+        m_run[i] = m_all;
+        l_run[i] = wsum;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[i][c] = o[c];
+      }
+    }
+    cluster_sync_all();  // peers stay resident until rank 0 has read their partials
+    if (rank != 0) return;
+  }
 #pragma unroll
   for (int i = 0; i < RT; ++i) {
     const int row = q0 + RT * ty + i;
@@ -701,28 +789,52 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
   }
 }
 
-template <int D, int BM>
+template <int D, int BM, int SPLIT>
 static cudaError_t launch_simt_tiled_bm(const SimtParams& p, cudaStream_t s) {
   const int DK = D + p.R;
+  // the split-KV partials (m double, l, acc: 12 + 4D bytes per row) reuse the K/V region
   const size_t smem = sizeof(float) * (static_cast<size_t>(DK) * (BM + 64) + 64 * D + BM * 68);
   static std::atomic<uint64_t> attr_mask{0};
-  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(fwd_simt_tiled_kernel<D, BM>), 200 * 1024);
+  auto kern = fwd_simt_tiled_kernel<D, BM, SPLIT>;
+  cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(kern), 200 * 1024);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.N + BM - 1) / BM, p.H, p.B);
-  fwd_simt_tiled_kernel<D, BM><<<grid, 256, smem, s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(((p.N + BM - 1) / BM) * SPLIT, p.H, p.B);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = SPLIT;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, p);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int D>
 static cudaError_t launch_simt_tiled(const SimtParams& p, cudaStream_t s) {
-  // 32-row CTAs when 64-row ones would not fill two waves of the 148 SMs
-  const int64_t ctas64 = static_cast<int64_t>((p.N + 63) / 64) * p.H * p.B;
-  return ctas64 < 2 * 148 ? launch_simt_tiled_bm<D, 32>(p, s) : launch_simt_tiled_bm<D, 64>(p, s);
+  // fill ~4 CTAs per SM: 64-row blocks, and a split-KV cluster of 2 / 4 / 8 CTAs per row block
+  // when there are too few row blocks (each CTA keeps >= 2 KV blocks of 64 keys)
+  const int64_t rowblocks = static_cast<int64_t>((p.N + 63) / 64) * p.H * p.B;
+  const int kvb = (p.M + 63) / 64;
+  if (rowblocks * 8 <= 4 * 148 && kvb >= 16) return launch_simt_tiled_bm<D, 64, 8>(p, s);
+  if (rowblocks * 4 <= 4 * 148 && kvb >= 8) return launch_simt_tiled_bm<D, 64, 4>(p, s);
+  if (rowblocks * 2 <= 4 * 148 && kvb >= 4) return launch_simt_tiled_bm<D, 64, 2>(p, s);
+  return launch_simt_tiled_bm<D, 64, 1>(p, s);
 }
 
 cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s) {
   const int DK = p.D + p.R;
-  if (DK <= 256 && (p.D == 32 || p.D == 64 || p.D == 128)) {
+  // the tiled kernel reads q / k / v rows as float4: 16-byte aligned rows only
+  auto al16 = [](const float* ptr, int64_t sn) {
+    return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0 && sn % 4 == 0;
+  };
+  const bool aligned = al16(p.q, p.q_sn) && al16(p.k, p.k_sn) && al16(p.v, p.v_sn) && p.q_sb % 4 == 0 &&
+                       p.q_sh % 4 == 0 && p.k_sb % 4 == 0 && p.k_sh % 4 == 0 && p.v_sb % 4 == 0 && p.v_sh % 4 == 0;
+  if (aligned && DK <= 256 && (p.D == 32 || p.D == 64 || p.D == 128)) {
     cudaError_t e = p.D == 32 ? launch_simt_tiled<32>(p, s)
                     : p.D == 64 ? launch_simt_tiled<64>(p, s) : launch_simt_tiled<128>(p, s);
     note_launch();
