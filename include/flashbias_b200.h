@@ -99,18 +99,24 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v,
                 fb_tensor* dv, fb_tensor* duq, fb_tensor* duk,
                 void* workspace, size_t workspace_bytes, void* stream);
 
-/* fb_attn_bwd with flags.  FB_BWD_DETERMINISTIC: the two-kernel backward
- * (dK'/dV key-stationary + dQ' query-stationary, no atomics): bitwise
- * reproducible run to run and across head shardings, at 7 GEMMs per tile
- * instead of 5.  The default (flags = 0) accumulates dQ with fp32 L2
- * reduce-adds whose order varies between runs. */
+/* fb_attn_bwd with a learnable dense bias and flags.
+ * dbias (nullable; requires bias): dB = dlogits/dbias = dS, written as
+ *   [B,H,N,M] in the bias dtype (rows contiguous, even row stride; the caller
+ *   zero-fills it for causal masks -- blocks above the diagonal are not
+ *   visited -- and sums it over dims the bias broadcasts).  Replaces the
+ *   reference's learnable-bias route (attention.py:187-188 with a trainable
+ *   DenseBias); head dim 64 / 128, fused backward only.
+ * FB_BWD_DETERMINISTIC: the two-kernel backward (dK'/dV key-stationary + dQ'
+ *   query-stationary, no atomics): bitwise reproducible run to run and across
+ *   head shardings, at 7 GEMMs per tile instead of 5.  The default (flags = 0)
+ *   accumulates dQ with fp32 L2 reduce-adds whose order varies between runs. */
 #define FB_BWD_DETERMINISTIC 1
 int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v,
                    const fb_tensor* uq, const fb_tensor* uk, const fb_tensor* bias,
                    const fb_tensor* o, const fb_tensor* lse, const fb_tensor* dout,
                    int mask, float scale, fb_tensor* dq, fb_tensor* dk,
-                   fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, int flags,
-                   void* workspace, size_t workspace_bytes, void* stream);
+                   fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, fb_tensor* dbias,
+                   int flags, void* workspace, size_t workspace_bytes, void* stream);
 
 size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k);
 

@@ -113,8 +113,8 @@ def attention_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, bias=None, mask="no
     ref SPEC.md:183).  With s = scale*(q k^T + premul fq fk^T) + bias,
     P = softmax(s), dP = dO V^T, dS = P (dP - rowsum(dO*O)):
       dq = scale dS k, dk = scale dS^T q, dv = P^T dO,
-      dfq = scale*premul dS fk, dfk = scale*premul dS^T fq
-    (factor gradients are summed over broadcast leading dims)."""
+      dfq = scale*premul dS fk, dfk = scale*premul dS^T fq, dbias = dS
+    (factor and bias gradients are summed over broadcast leading dims)."""
     q, k, v, do = (np.asarray(x, dtype=np.float64) for x in (q, k, v, do))
     scale = 1.0 / math.sqrt(q.shape[-1]) if scale is None else scale
     s = _logits(q, k, None if fq is None else np.asarray(fq, np.float64),
@@ -136,6 +136,8 @@ def attention_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, bias=None, mask="no
         "dk": scale * np.swapaxes(ds, -1, -2) @ q,
         "dv": np.swapaxes(p, -1, -2) @ do,
     }
+    if bias is not None:  # the bias enters the logits unscaled: dlogits/dbias = dS (summed where it broadcasts)
+        res["dbias"] = _reduce_to(ds, np.shape(bias))
     if fq is not None:
         fq = np.asarray(fq, np.float64)
         fk = np.asarray(fk, np.float64)

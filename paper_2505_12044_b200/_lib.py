@@ -49,8 +49,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     sig = {
         "fb_attn_fwd": (i32, [_P, _P, _P, _P, _P, _P, i32, f32, _P, _P, vp]),
         "fb_attn_bwd": (i32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, i32, f32, _P, _P, _P, _P, _P, vp, sz, vp]),
-        "fb_attn_bwd_ex": (i32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, i32, f32, _P, _P, _P, _P, _P, i32, vp, sz,
-                                 vp]),
+        "fb_attn_bwd_ex": (i32, [_P, _P, _P, _P, _P, _P, _P, _P, _P, i32, f32, _P, _P, _P, _P, _P, _P, i32, vp,
+                                 sz, vp]),
         "fb_bwd_workspace_bytes": (sz, [_P, _P]),
         "fb_prepare_factors": (i32, [_P, i32, i32, f32, _P, vp]),
         "fb_factor_rpad": (i64, [i64, i32]),

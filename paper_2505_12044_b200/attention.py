@@ -387,7 +387,8 @@ def _fwd_launch(q, k, v, uq, uk, bias, mask_code, scale, need_lse=True):
 FB_BWD_DETERMINISTIC = 1
 
 
-def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad, deterministic=False):
+def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad, deterministic=False,
+                want_dbias=False):
     import torch
     lib = _lib.lib()
     D = _lib.desc
@@ -400,16 +401,21 @@ def _bwd_launch(q, k, v, uq, uk, bias, o, lse, do, mask_code, scale, want_fgrad,
             B, H = q.shape[0], q.shape[1]
             duq = torch.empty(B, H, q.shape[2], uq.shape[-1], dtype=torch.float32, device=q.device)
             duk = torch.empty(B, H, k.shape[2], uk.shape[-1], dtype=torch.float32, device=q.device)
+        db = None
+        if want_dbias:  # [B,H,N,M] in the bias dtype, even row stride; causal blocks above the diagonal stay 0
+            B, H, N, M = q.shape[0], q.shape[1], q.shape[2], k.shape[2]
+            alloc = torch.zeros if mask_code == 1 else torch.empty
+            db = alloc(B, H, N, M + (M & 1), dtype=bias.dtype, device=q.device)[..., :M]
         dq_d, k_d = D(q), D(k)
         ws_bytes = int(lib.fb_bwd_workspace_bytes(_lib.ref(dq_d), _lib.ref(k_d)))
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=q.device)
         _lib.check(lib.fb_attn_bwd_ex(_lib.ref(D(q)), _lib.ref(D(k)), _lib.ref(D(v)), _lib.ref(D(uq)),
                                       _lib.ref(D(uk)), _lib.ref(D(bias)), _lib.ref(D(o)), _lib.ref(D(lse)),
                                       _lib.ref(D(do)), mask_code, float(scale), _lib.ref(D(dq)), _lib.ref(D(dk)),
-                                      _lib.ref(D(dv)), _lib.ref(D(duq)), _lib.ref(D(duk)),
+                                      _lib.ref(D(dv)), _lib.ref(D(duq)), _lib.ref(D(duk)), _lib.ref(D(db)),
                                       FB_BWD_DETERMINISTIC if deterministic else 0, ws.data_ptr(), ws_bytes,
                                       _lib.stream_ptr(q.device)))
-    return dq, dk, dv, duq, duk
+    return dq, dk, dv, duq, duk, db
 
 
 def _make_fn():
@@ -432,17 +438,20 @@ def _make_fn():
         def backward(ctx, do):
             q, k, v, uq, uk, bias, o, lse, fq, fk = ctx.saved_tensors
             mask_code, scale, premul, split, deterministic = ctx.cfg
-            if bias is not None and ctx.needs_input_grad[5]:
-                raise NotImplementedError("gradient w.r.t. a dense bias is not produced (static bias)")
+            want_db = bias is not None and ctx.needs_input_grad[5]
             want_fg = fq is not None and (ctx.needs_input_grad[3] or ctx.needs_input_grad[4])
-            dq, dk, dv, duq, duk = _bwd_launch(q, k, v, uq, uk, bias, o, lse, do.contiguous(), mask_code, scale,
-                                               want_fg, deterministic)
+            dq, dk, dv, duq, duk, db = _bwd_launch(q, k, v, uq, uk, bias, o, lse, do.contiguous(), mask_code,
+                                                   scale, want_fg, deterministic, want_db)
+            if db is not None:  # learnable dense bias: sum dS over the dims the bias broadcasts
+                dims = [i for i in (0, 1) if bias.shape[i] == 1 and db.shape[i] != 1]
+                if dims:
+                    db = db.sum(dim=dims, keepdim=True)
             dfq = dfk = None
             if want_fg:
                 # the kernel's duq is d/d(uq) of scale*uq.uk; uq = premul*fq -> dfq = premul*duq
                 dfq = fold_factor_grads(duq, fq, 0, split, premul).to(fq.dtype)
                 dfk = fold_factor_grads(duk, fk, 1, split, 1.0).to(fk.dtype)
-            return dq, dk, dv, dfq, dfk, None, None, None, None, None, None
+            return dq, dk, dv, dfq, dfk, db, None, None, None, None, None
 
     return FlashBiasFunction
 

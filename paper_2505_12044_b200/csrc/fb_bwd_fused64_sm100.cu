@@ -334,6 +334,9 @@ __global__ void __launch_bounds__(512, 1)
           pk[c2] = pack2<BF16>(ds.x, ds.y);
         }
       }
+      if constexpr (DENSE) {
+        if (p.dbias != nullptr) store_dbias_rows(p, b, h, q0, kv, lane, pk);
+      }
       tmem_st32(t_dpt, pk);
       if (u >= 1) mbar_wait(&bars->dsbuf_free[g], (u - 1) & 1);
       uint8_t* row = ds_buf + g * Cfg::kDsBuf + r * 128;

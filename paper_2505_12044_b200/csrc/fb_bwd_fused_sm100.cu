@@ -369,6 +369,9 @@ __global__ void __launch_bounds__(512, 1)
           pk[c2] = pack2<BF16>(ds.x, ds.y);
         }
       }
+      if constexpr (DENSE) {
+        if (p.dbias != nullptr) store_dbias_rows(p, b, h, q0, kv, lane, pk);
+      }
       tmem_st32(t_dpt, pk);
       // dS^T row -> shared memory (B operand of dQ^T), SW128 MN-major: 16-byte
       // chunk ch of row r lives at chunk ch ^ (r & 7)

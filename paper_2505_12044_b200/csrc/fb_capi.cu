@@ -322,15 +322,15 @@ int fb_attn_bwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
                 const fb_tensor* dout, int mask, float scale, fb_tensor* dq, fb_tensor* dk,
                 fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, void* workspace,
                 size_t workspace_bytes, void* stream) {
-  return fb_attn_bwd_ex(q, k, v, uq, uk, bias, o, lse, dout, mask, scale, dq, dk, dv, duq, duk, 0, workspace,
-                        workspace_bytes, stream);
+  return fb_attn_bwd_ex(q, k, v, uq, uk, bias, o, lse, dout, mask, scale, dq, dk, dv, duq, duk, nullptr, 0,
+                        workspace, workspace_bytes, stream);
 }
 
 int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, const fb_tensor* uq,
                    const fb_tensor* uk, const fb_tensor* bias, const fb_tensor* o, const fb_tensor* lse,
                    const fb_tensor* dout, int mask, float scale, fb_tensor* dq, fb_tensor* dk,
-                   fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, int flags, void* workspace,
-                   size_t workspace_bytes, void* stream) {
+                   fb_tensor* dv, fb_tensor* duq, fb_tensor* duk, fb_tensor* dbias, int flags,
+                   void* workspace, size_t workspace_bytes, void* stream) {
   int rc;
   if (flags & ~FB_BWD_DETERMINISTIC) return fail(FB_EVALUE, "unknown backward flags 0x%x", flags);
   if ((rc = check_qkv(q, k, v))) return rc;
@@ -354,6 +354,14 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
     rp = (int)(rpad / 16);
   }
   if (bias && uq) return fail(FB_ECONFIG, "either factors or a dense bias, not both");
+  if (dbias) {
+    if (!bias) return fail(FB_EVALUE, "dbias requested without a dense bias");
+    if (dbias->dtype != bias->dtype) return fail(FB_EVALUE, "dbias dtype must match the bias");
+    if (dbias->shape[0] != B || dbias->shape[1] != H || dbias->shape[2] != N || dbias->shape[3] != M)
+      return fail(FB_ESHAPE, "dbias must be [B,H,N,M] (reduce broadcast dims on the host)");
+    if (dbias->stride[3] != 1 || dbias->stride[2] % 2 || reinterpret_cast<uintptr_t>(dbias->data) % 4)
+      return fail(FB_ESHAPE, "dbias rows must be contiguous with an even, 4-byte aligned row stride");
+  }
   if (bias && (bias->stride[2] * 2) % 16) return fail(FB_ECONFIG, "dense bias rows must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // preprocess delta = rowsum(dO * O)
@@ -411,6 +419,10 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
     p.uk_bb = uk->shape[0] == 1; p.uk_hb = uk->shape[1] == 1;
   }
   if (bias) { p.bias_bb = bias->shape[0] == 1; p.bias_hb = bias->shape[1] == 1; }
+  if (dbias) {
+    Tensor4 td = to_t4(dbias);
+    p.dbias = dbias->data; p.db_sb = td.stride[0]; p.db_sh = td.stride[1]; p.db_sn = td.stride[2];
+  }
   trace_target(&p.trace, &p.trace_cta);
   static const int force_split = [] {
     const char* v = getenv("FB_FORCE_SPLIT_BWD");
@@ -420,6 +432,9 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
   // backward: no atomics, every gradient element written once in a fixed order
   const bool deterministic = force_split || (flags & FB_BWD_DETERMINISTIC);
   const bool fused = !deterministic && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
+  if (dbias && !fused)
+    return fail(FB_ECONFIG, "the dense-bias gradient is produced by the fused backward (head dim 64/128, "
+                            "not deterministic)");
   if (fused) {
     float* acc = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(delta) +
                                           ((size_t)B * H * N * sizeof(float) + 255) / 256 * 256);

@@ -59,8 +59,35 @@ struct BwdParams {
   float* duk; int64_t duk_sb, duk_sh, duk_sn;
   int uq_bb, uq_hb, uk_bb, uk_hb, bias_bb, bias_hb;
   float* dq_acc; int acc_n4;  // 128x128-tile kernel: transposed fp32 dQ accumulator [B,H,128,acc_n4]
+  void* dbias; int64_t db_sb, db_sh, db_sn;  // nullable: learnable dense bias gradient [B,H,N,M] (bias dtype)
   unsigned long long* trace; int trace_cta;  // FB_TRACE builds only
 };
+
+#ifdef __CUDACC__
+// Learnable dense bias (K4): dB[b,h,q,kv] = dS[q,kv] (the bias enters the logits
+// unscaled, ref attention.py:187-188).  pk[c2] holds the 16-bit dS of queries
+// q0+2c2, q0+2c2+1 for this thread's key kv; neighbouring lanes hold
+// neighbouring keys, so lane pairs swap halves and every lane stores one
+// 4-byte (kv, kv+1) pair of one query row: a warp writes 64 contiguous bytes of
+// two dB rows per store.  Rows are 4-byte aligned (db_sn even, host-padded).
+__device__ __forceinline__ void store_dbias_rows(const BwdParams& p, int b, int h, int q0, int kv, int lane,
+                                                 const uint32_t (&pk)[32]) {
+  uint16_t* base = static_cast<uint16_t*>(p.dbias) + static_cast<int64_t>(b) * p.db_sb +
+                   static_cast<int64_t>(h) * p.db_sh;
+  const int odd = lane & 1, kve = kv & ~1;
+#pragma unroll
+  for (int c2 = 0; c2 < 32; ++c2) {
+    const uint32_t mine = pk[c2], other = __shfl_xor_sync(0xffffffffu, pk[c2], 1);
+    const uint32_t w = odd ? __byte_perm(other, mine, 0x7632) : __byte_perm(mine, other, 0x5410);
+    const int q = q0 + 2 * c2 + odd;
+    if (q < p.N && kve < p.M) {
+      uint16_t* dst = base + static_cast<int64_t>(q) * p.db_sn + kve;
+      if (kve + 1 < p.M) *reinterpret_cast<uint32_t*>(dst) = w;
+      else *dst = static_cast<uint16_t>(w & 0xffffu);
+    }
+  }
+}
+#endif
 
 struct BwdMaps {
   // dKV kernel: streamed 64-row query-side boxes, resident 128-row key side

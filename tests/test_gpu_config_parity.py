@@ -194,3 +194,38 @@ def test_deterministic_backward_is_bitwise_and_shard_invariant(D, R):
                             fk=_np(fk[0, 0]), premul=math.sqrt(D), mask="causal")
     _check_head({"o": _np(a[0][0, 0]), "dq": _np(a[1][0, 0]), "dk": _np(a[2][0, 0]), "dv": _np(a[3][0, 0])}, ref,
                 ("o", "dq", "dk", "dv"), "deterministic head 0")
+
+
+@pytest.mark.parametrize("D,causal,M,bcast", [(128, False, 384, False), (128, True, 256, False), (64, False, 333, False),
+                                              (64, True, 192, True)])
+def test_learnable_dense_bias_gradient(D, causal, M, bcast):
+    """K4 with a learnable dense bias: dB = dS written by the fused backward
+    (ref attention.py:187-188 with a trainable bias), summed over a batch-
+    broadcast bias, against the oracle's analytic dbias."""
+    B, H = 2, 2
+    N = M if causal else 320
+    q = _rand((B, H, N, D), 11)
+    k, v = _rand((B, H, M, D), 12), _rand((B, H, M, D), 13)
+    do = _rand((B, H, N, D), 14)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    bias = (torch.randn(1 if bcast else B, H, N, M, generator=g, device="cuda") * 2).bfloat16().float()
+    bias.requires_grad_(True)
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    mask = "causal" if causal else "none"
+    o = fb.tiled_attention(q, k, v, fb.DenseBias(bias), mask=mask)
+    dq, dk, dv, db = torch.autograd.grad(o, (q, k, v, bias), do)
+    assert db.shape == bias.shape and db.dtype == bias.dtype
+    for b in range(B):
+        for h in range(H):
+            ref = orc.attention_bwd(_np(q[b, h]), _np(k[b, h]), _np(v[b, h]), _np(do[b, h]),
+                                    bias=_np(bias[0 if bcast else b, h]), mask=mask)
+            got = {"o": _np(o[b, h]), "dq": _np(dq[b, h]), "dk": _np(dk[b, h]), "dv": _np(dv[b, h])}
+            _check_head(got, ref, ("o", "dq", "dk", "dv"), f"dense learnable b{b} h{h}")
+            if not bcast:
+                _check_head({"dbias": _np(db[b, h])}, ref, ("dbias",), f"dbias b{b} h{h}")
+    if bcast:
+        for h in range(H):
+            tot = sum(orc.attention_bwd(_np(q[b, h]), _np(k[b, h]), _np(v[b, h]), _np(do[b, h]),
+                                        bias=_np(bias[0, h]), mask=mask)["dbias"] for b in range(B))
+            _check_head({"dbias": _np(db[0, h])}, {"dbias": tot}, ("dbias",), f"dbias summed h{h}")
