@@ -285,6 +285,11 @@ def reference_svd_report(cfg, n_heads: int = 1):
     return t
 
 
+def learnable(cfg) -> bool:
+    """Bias learnable on both arms: C2's spatial weights by default, --learnable elsewhere."""
+    return cfg["bwd"] and not cfg.get("static") and (cfg["bias"] == "spatial" or cfg.get("learnable", False))
+
+
 def step_fn(cfg, inp, mode: str):
     """One pass of the hot path: forward (+ backward) through the public API."""
     import paper_2505_12044_b200 as fb
@@ -294,9 +299,11 @@ def step_fn(cfg, inp, mode: str):
         q.requires_grad_(True)
         k.requires_grad_(True)
         v.requires_grad_(True)
-        if cfg["bias"] == "spatial" and mode == "flashbias" and not cfg.get("static"):
+        if learnable(cfg) and mode == "flashbias":  # learnable bias: factor gradients dfq / dfk
             inp["fq"].requires_grad_(True)
             inp["fk"].requires_grad_(True)
+        if learnable(cfg) and mode == "dense":  # the same bias learnable on the dense arm: dB = dS
+            inp["dense"].requires_grad_(True)
 
     def run():
         if mode == "flashbias":
@@ -304,7 +311,7 @@ def step_fn(cfg, inp, mode: str):
         else:
             out = fb.tiled_attention(q, k, v, fb.DenseBias(inp["dense"]), mask=mask)
         if cfg["bwd"]:
-            cands = (q, k, v, inp["fq"], inp["fk"]) if mode == "flashbias" else (q, k, v)
+            cands = (q, k, v, inp["fq"], inp["fk"]) if mode == "flashbias" else (q, k, v, inp["dense"])
             grads = [t for t in cands if t is not None and t.requires_grad]
             import torch
             torch.autograd.grad(out, grads, inp["do"])
@@ -390,7 +397,7 @@ def kernel_breakdown(cfg, inp, reps: int = 3):
         o, lse = A._fwd_launch(q, k, v, uq, uk, None, mask_code, scale)
         ev[1].record()
         if cfg["bwd"]:
-            A._bwd_launch(q, k, v, uq, uk, None, o, lse, do, mask_code, scale, False)
+            A._bwd_launch(q, k, v, uq, uk, None, o, lse, do, mask_code, scale, learnable(cfg))
         ev[2].record()
         torch.cuda.synchronize()
         fwd_ms.append(ev[0].elapsed_time(ev[1]))
@@ -943,8 +950,10 @@ def main():
     ap.add_argument("--ref-full-heads", type=int, default=1,
                     help="--impl reference: also time one whole head per core (per-head medians)")
     ap.add_argument("--no-graph", action="store_true", help="never CUDA-graph the step (small configs use graphs)")
+    ap.add_argument("--learnable", action="store_true",
+                    help="C4/C5: learnable bias on both arms (FlashBias dfq/dfk vs dense dB); C2 is learnable by default")
     ap.add_argument("--static-factors", action="store_true",
-                    help="C2: treat the spatial factors as a fixed bias (no factor gradients), like the dense arm")
+                    help="C2: treat the spatial bias as fixed on both arms (no factor / bias gradients)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.config == "MIX":
@@ -956,6 +965,13 @@ def main():
         if "R" not in cfg:
             ap.error("--rank applies to the SVD configs C4/C5")
         cfg["R"] = args.rank
+    if args.learnable:
+        if args.config == "C3":
+            ap.error("--learnable: C3's dense bias is shared by the 4 batch rows; its dB would be a 68 GB "
+                     "per-batch buffer reduced on the host -- use C5 (per-(b,h) biases)")
+        cfg["learnable"] = True
+        cfg["bwd"] = True
+        cfg["desc"] += " [learnable bias: FlashBias dfq/dfk vs dense dB]"
     if args.static_factors:
         cfg["static"] = True
         cfg["desc"] += " [static factors: no factor gradients]"
