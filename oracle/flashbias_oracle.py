@@ -195,6 +195,28 @@ def blocked_attention_fwd_bwd(q, k, v, do, fq=None, fk=None, premul=1.0, mask="n
     return res
 
 
+def chunk_attention_bwd(q, k, v, do, o, lse, fq=None, fk=None, premul=1.0, mask="none", scale=None):
+    """The backward of one (query chunk, key chunk) pair of a sequence split
+    across ranks (ring attention), given the GLOBAL output rows ``o`` and
+    log-sum-exps ``lse`` of the query chunk: P = exp(S - lse) is then the
+    exact slice of the global softmax, so the pair's dq / dk / dv / dfq / dfk
+    are the exact contributions of that slice to attention_bwd's gradients."""
+    q, k, v, do, o = (np.asarray(x, dtype=np.float64) for x in (q, k, v, do, o))
+    scale = 1.0 / math.sqrt(q.shape[-1]) if scale is None else scale
+    s = _logits(q, k, None if fq is None else np.asarray(fq, np.float64),
+                None if fk is None else np.asarray(fk, np.float64), premul, None, scale)
+    if mask == "causal":
+        n, m = s.shape[-2:]
+        s = np.where(np.triu(np.ones((n, m), dtype=bool), k=1), -np.inf, s)
+    p = np.exp(s - np.asarray(lse, np.float64)[..., None])
+    ds = p * (do @ np.swapaxes(v, -1, -2) - (do * o).sum(axis=-1, keepdims=True))
+    res = {"dq": scale * ds @ k, "dk": scale * np.swapaxes(ds, -1, -2) @ q, "dv": np.swapaxes(p, -1, -2) @ do}
+    if fq is not None:
+        res["dfq"] = scale * premul * ds @ np.asarray(fk, np.float64)
+        res["dfk"] = scale * premul * np.swapaxes(ds, -1, -2) @ np.asarray(fq, np.float64)
+    return res
+
+
 def _reduce_to(x, shape):
     """Sum x over dims where ``shape`` broadcasts (size 1 / missing)."""
     while x.ndim > len(shape):
