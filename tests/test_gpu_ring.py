@@ -9,7 +9,6 @@ import math
 import pytest
 import torch
 
-import bench
 import paper_2505_12044_b200 as fb
 from oracle import flashbias_oracle as orc
 from paper_2505_12044_b200 import attention as A
@@ -29,8 +28,10 @@ def test_thread_ring_matches_oracle(G, D, mask):
     N = Nc * G
     g = torch.Generator(device="cuda").manual_seed(G * 10 + D)
     q, k, v, do = (torch.randn(1, H, N, D, generator=g, device="cuda").bfloat16() for _ in range(4))
-    slopes = bench.alibi_slopes(8)[:H]
-    fq, fk = fb.alibi_factors(slopes, N, N)  # global positions: each chunk keeps its rows' factors
+    # well-conditioned learnable factors (ALiBi's position-sized factor gradients cancel to ~0 and are not a
+    # meaningful bf16 parity target); each chunk keeps its own rows' factors, which travel with K
+    fq = (torch.randn(1, H, N, 8, generator=g, device="cuda") * 0.4).contiguous()
+    fk = (torch.randn(1, H, N, 8, generator=g, device="cuda") * 0.4).contiguous()
     scale = 1 / math.sqrt(D)
     outs = {}
 
@@ -69,7 +70,8 @@ def test_ring_autograd_on_one_rank_equals_single_call():
     N, H, D = 384, 2, 128
     g = torch.Generator(device="cuda").manual_seed(3)
     q, k, v, do = (torch.randn(2, H, N, D, generator=g, device="cuda").bfloat16() for _ in range(4))
-    fq, fk = fb.alibi_factors(bench.alibi_slopes(8)[:H], N, N)
+    fq = (torch.randn(1, H, N, 4, generator=g, device="cuda") * 0.4).contiguous()
+    fk = (torch.randn(1, H, N, 4, generator=g, device="cuda") * 0.4).contiguous()
     res = []
     for ring in (True, False):
         qq, kk, vv = (t.clone().requires_grad_(True) for t in (q, k, v))
@@ -77,5 +79,8 @@ def test_ring_autograd_on_one_rank_equals_single_call():
         o = (fb.ring_flashbias_attention(qq, kk, vv, f1, f2, mask="causal", comm=SoloRing()) if ring
              else fb.flashbias_attention(qq, kk, vv, f1, f2, mask="causal"))
         res.append([o.detach()] + list(torch.autograd.grad(o, (qq, kk, vv, f1, f2), do)))
-    for a, b in zip(*res):
-        assert torch.allclose(a.float(), b.float(), rtol=1e-3, atol=1e-3 * float(b.float().abs().max()))
+    # same kernels; the ring plans its factor split from the rank alone (shard-invariant), so the two
+    # paths may use different split levels: agreement at the bf16 level, not bitwise
+    for name, a, b in zip(("o", "dq", "dk", "dv", "dfq", "dfk"), *res):
+        err = float((a.double() - b.double()).abs().max() / b.double().abs().max())
+        assert err < TOL, (name, err)
