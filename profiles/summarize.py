@@ -3,7 +3,7 @@
 into profiles/ncu_<tag>.md and profiles/ncu_traffic.json (per-launch DRAM bytes
 consumed by bench.py's roofline.traffic).
 
-    python profiles/summarize.py r01b
+    python profiles/summarize.py r02 C3
 """
 
 import csv
@@ -31,6 +31,11 @@ METRICS = [
     ("l1tex__m_l1tex2xbar_write_bytes.sum.pct_of_peak_sustained_elapsed", "SM->L2 write % of peak"),
     ("l1tex__m_xbar2l1tex_read_bytes.sum", "L2->SM read bytes (TMA loads)"),
     ("lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum", "L2 read hits (sectors)"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/smem throughput % (active)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem LSU wavefronts % of peak"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput % of peak"),
+    ("lts__t_sectors_op_red.sum", "L2 reduction sectors"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
     ("launch__registers_per_thread", "registers/thread"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("launch__grid_size", "grid"),
@@ -55,14 +60,14 @@ def to_num(v, u):
     return x * UNITS.get(u, 1)
 
 
-def main(tag):
-    lines = [f"# ncu summary — {tag}", "",
-             "Captured with `profiles/run_ncu.sh` on one B200 (`--set full --clock-control none`), C3 "
-             "workload (B=4 H=32 N=16384 d=128 bf16 causal ALiBi), one launch per kernel after warm-up. "
+def main(tag, cfg):
+    lines = [f"# ncu summary — {tag}, {cfg}", "",
+             f"Captured with `profiles/run_ncu.sh {tag} {cfg}` on one B200 (`--set full --clock-control none`), "
+             f"bench.py workload {cfg}, one launch per kernel after warm-up. "
              "ncu replays each kernel ~40x with cold caches: compare shares/ratios, not absolute times.", ""]
     traffic = {}
-    for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_*.ncu-rep"))):
-        name = os.path.basename(rep)[len(f"prof_{tag}_"):-len(".ncu-rep")]
+    for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_{cfg}_*.ncu-rep"))):
+        name = os.path.basename(rep)[len(f"prof_{tag}_{cfg}_"):-len(".ncu-rep")]
         m = raw(rep)
         lines += [f"## {name}", "", "| metric | value |", "|---|---|"]
         got = {}
@@ -77,7 +82,7 @@ def main(tag):
             traffic[kind] = rd + wr
             lines.append(f"| DRAM read+write per launch | {(rd + wr) / 1e9:.2f} GB |")
         lines.append("")
-    lf = os.path.join(OUT, f"launches_{tag}.csv")
+    lf = os.path.join(OUT, f"launches_{tag}_{cfg}.csv")
     if os.path.exists(lf):
         rows = list(csv.reader(open(lf)))
         hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -89,18 +94,19 @@ def main(tag):
                 k = r[ki].split("(")[0].replace("void ", "")
                 tot[k] = tot.get(k, 0.0) + to_num(r[vi], r[ui])
         s = sum(tot.values())
-        lines += ["## launch list (every kernel of one C3 bench step: bench.py --steps 1 --warmup 1, cold-cache serialised replays)", "", "| kernel | total time | share |",
+        lines += [f"## launch list (every kernel of one {cfg} bench step: bench.py --steps 1 --warmup 1, cold-cache "
+                  "serialised replays)", "", "| kernel | total time | share |",
                   "|---|---|---|"]
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
             lines.append(f"| `{k}` | {v * 1e3:.2f} ms | {v / s:.1%} |")
         lines.append("")
-    open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w").write("\n".join(lines))
+    open(os.path.join(ROOT, "profiles", f"ncu_{tag}_{cfg}.md"), "w").write("\n".join(lines))
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     data = json.load(open(tj)) if os.path.exists(tj) else {}
-    data["C3"] = {**data.get("C3", {}), **traffic, "tag": tag}
+    data[cfg] = {**data.get(cfg, {}), **traffic, "tag": tag}
     json.dump(data, open(tj, "w"), indent=1)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
+    main(sys.argv[1] if len(sys.argv) > 1 else "r02", sys.argv[2] if len(sys.argv) > 2 else "C3")
