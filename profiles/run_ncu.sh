@@ -1,7 +1,7 @@
 #!/bin/bash
 # Profiling recipe used for profiles/ (run under gpurun on one B200).
 #   bash profiles/run_ncu.sh <tag> <config> [extra bench.py args]
-# 1) launch list with device times of one bench step of <config> (cold-cache, serialised)
+# 1) launch list with device times of the bench steps of <config> (cold-cache, serialised)
 # 2) one --set full capture of the step's forward kernel and of its backward kernel
 set -e
 mkdir -p gpurun_out
@@ -9,10 +9,13 @@ TAG=${1:-r02}
 CFG=${2:-C3}
 shift 2 || true
 ARGS="--config $CFG --steps 1 --warmup 1 --skip-dense --skip-e2e --skip-cpu --skip-sdpa --ref-svd-heads 0 --no-graph $*"
-ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+# only the timed bench steps are profiled (BENCH_PROFILE_RANGE=1 brackets them with cudaProfilerStart/Stop), so the
+# setup (input generation, the device SVD of C4/C5: cuSOLVER kernels ncu cannot replay) stays outside
+export BENCH_PROFILE_RANGE=1
+ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}_${CFG}.csv python bench.py $ARGS > gpurun_out/launches_${TAG}_${CFG}.log 2>&1
 for K in fb_fwd_kernel "fb_bwd_(t128|fused|fused64|dkv)_kernel"; do
   NAME=$( [ "$K" = fb_fwd_kernel ] && echo fwd || echo bwd )
-  ncu --set full --clock-control none --import-source on -k "regex:${K}" -s 1 -c 1 \
+  ncu --profile-from-start off --set full --clock-control none --import-source on -k "regex:${K}" -s 1 -c 1 \
       -o gpurun_out/prof_${TAG}_${CFG}_${NAME} -f python bench.py $ARGS > /dev/null 2>&1 || true
 done
