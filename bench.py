@@ -588,6 +588,8 @@ def run_gpu(args, cfg):
 
 
 def dense_note(cfg) -> str:
+    if cfg.get("dense_unavailable"):
+        return cfg["dense_unavailable"]
     base = "our dense-bias arm (K3/K4, same pipeline) streams the bias as a bf16 [Bb,H,N,N] tensor"
     if cfg.get("bias") == "alibi" and cfg["N"] > 4096:
         return (base + f"; with ALiBi at N={cfg['N']} |b| reaches ~{int(cfg['N'] * 0.84)}, where bf16 spacing is "
@@ -977,9 +979,10 @@ def main():
             ap.error("--rank applies to the SVD configs C4/C5")
         cfg["R"] = args.rank
     if args.learnable:
-        if args.config == "C3":
-            ap.error("--learnable: C3's dense bias is shared by the 4 batch rows; its dB would be a 68 GB "
-                     "per-batch buffer reduced on the host -- use C5 (per-(b,h) biases)")
+        if args.config == "C3":  # FlashBias arm only: learnable ALiBi factors (the 128x128-tile LEARN kernel)
+            args.skip_dense = True
+            cfg["dense_unavailable"] = ("learnable dense arm not run: C3's dB = dS is a [4,32,16384,16384] bf16 "
+                                        "buffer (68 GB) per step")
         cfg["learnable"] = True
         cfg["bwd"] = True
         cfg["desc"] += " [learnable bias: FlashBias dfq/dfk vs dense dB]"

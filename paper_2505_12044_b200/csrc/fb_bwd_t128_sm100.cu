@@ -39,6 +39,16 @@
 // load traffic leaves more of it to the reductions.  Causal: both CTAs start
 // at the even tile's diagonal block; for the odd tile that first block is
 // fully masked (P = dS = 0) and its dQ reduction is skipped.
+//
+// LEARN variant (learnable factors, one 16-column panel): the factor gradients
+// dUk = scale dS^T Uq and dUq = scale dS Uk are two extra N = 16 MMAs per block.
+// TMEM has no free columns for a dUk accumulator (S^T | dP^T | dV | dK fill all
+// 512), so both land in the dP^T columns once the elementwise warps have read
+// dP^T: the drain adds the 16 dUk columns into registers (written at the end,
+// one fp32 row per key) and reduce-adds the 128 x 16 dUq block into the fp32
+// dUq output like a 9th dQ chunk.  MMA order per block becomes
+//   S(j+1) | dUk(j) dUq(j) dK(j) | dQ^T(j) | dP(j+1) dV(j+1)
+// with dQ^T(j) issued once the drain has read the factor columns.
 #include "fb_kernels.h"
 #include "fb_sm100.cuh"
 
@@ -106,15 +116,18 @@ struct T128Bars {
   uint64_t q_full[2], q_empty[2];
   uint64_t do_full, do_empty;
   uint64_t s_full, p_ready, dp_full, ds_ready, ds_free, dq_full, dq_free, final_;
+  uint64_t fg_full, fg_free;  // LEARN: factor-gradient columns written / read out of the dP^T region
   uint32_t tmem_base;
 };
 
-template <int RP, bool BF16, bool MC>
+template <int RP, bool BF16, bool MC, bool LEARN>
 __global__ void __launch_bounds__(512, 1)
     fb_bwd_t128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_uq, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_uk,
-                       const __grid_constant__ CUtensorMap tm_dqacc, const BwdParams p) {
+                       const __grid_constant__ CUtensorMap tm_dqacc, const __grid_constant__ CUtensorMap tm_duq,
+                       const BwdParams p) {
+  static_assert(!LEARN || RP == 1, "factor gradients: one 16-column panel");
   using Cfg = T128Cfg<RP>;
   constexpr int D = 128;
   extern __shared__ uint8_t smem_raw[];
@@ -145,6 +158,7 @@ __global__ void __launch_bounds__(512, 1)
     tma_prefetch(&tm_k);
     tma_prefetch(&tm_v);
     tma_prefetch(&tm_dqacc);
+    if (LEARN) tma_prefetch(&tm_duq);
     if (RP > 0) {
       tma_prefetch(&tm_uq);
       tma_prefetch(&tm_uk);
@@ -164,6 +178,8 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(&bars->dq_full, 1);
     mbar_init(&bars->dq_free, 4);
     mbar_init(&bars->final_, 1);
+    mbar_init(&bars->fg_full, 1);
+    mbar_init(&bars->fg_free, 4);
     fence_barrier_init();
   }
   if (warp == 13) tmem_alloc<512>(&bars->tmem_base);
@@ -266,22 +282,52 @@ __global__ void __launch_bounds__(512, 1)
         if constexpr (MC) tc_commit_mc(&bars->do_empty, kPair);
         else tc_commit(&bars->do_empty);
       };
-      auto issue_dqk = [&](int j) {
-        mbar_wait(&bars->ds_ready, j & 1);
-        tc_fence_after();
-        trace(p.trace, p.trace_cta, 13, j);
+      // 16-column factor panel (rows = K index, SW32) as an MN-major operand: K-step = 16 rows x 32 B
+      auto panel_mn = [&](int off) { return make_sdesc(opaque_u32(sbase) + off, 128 * 32, 8 * 32, 6); };
+      constexpr uint64_t kPanelRow16 = 16 * 32 >> 4;
+      auto issue_dq = [&](int j) {
         const uint64_t dm_kt = desc(Cfg::kK, true), dm_ds = desc(Cfg::kDS, true);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T (K = 128 keys) into the dP^T columns
           mma_ss(tmem + T_DP, dm_kt + kk * kRow16, dm_ds + kk * kRow16, id_q, kk > 0 ? 1u : 0u);
         tc_commit(&bars->dq_full);
+        (void)j;
+      };
+      auto issue_dk = [&](int j) {
         trace(p.trace, p.trace_cta, 12, j);
         const uint64_t dm_q = desc(qslot(j), true), dk_ds = desc(Cfg::kDS, false);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dK += dS^T Q (K = 128 queries)
           mma_ss(tmem + T_DK, dk_ds + ks(kk), dm_q + kk * kRow16, id_d, (j > 0 || kk > 0) ? 1u : 0u);
-        if constexpr (MC) tc_commit_mc(&bars->q_empty[j & 1], kPair);
-        else tc_commit(&bars->q_empty[j & 1]);
+      };
+      auto issue_dqk = [&](int j) {
+        mbar_wait(&bars->ds_ready, j & 1);
+        tc_fence_after();
+        trace(p.trace, p.trace_cta, 13, j);
+        if constexpr (LEARN) {
+          constexpr uint32_t id_fk = make_idesc(128, 16, false, true, BF16);  // dUk part = dS^T Uq
+          constexpr uint32_t id_fq = make_idesc(128, 16, true, true, BF16);   // dUq = dS Uk (A = dS^T read MN-major)
+          const uint64_t dk_ds = desc(Cfg::kDS, false), dm_ds = desc(Cfg::kDS, true);
+          const uint64_t uq_mn = panel_mn(qslot(j) + Cfg::kTile), uk_mn = panel_mn(Cfg::kUk);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(tmem + T_DP, dk_ds + ks(kk), uq_mn + kk * kPanelRow16, id_fk, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(tmem + T_DP + 16, dm_ds + kk * kRow16, uk_mn + kk * kPanelRow16, id_fq, kk > 0 ? 1u : 0u);
+          tc_commit(&bars->fg_full);
+          issue_dk(j);
+          if constexpr (MC) tc_commit_mc(&bars->q_empty[j & 1], kPair);
+          else tc_commit(&bars->q_empty[j & 1]);
+          mbar_wait(&bars->fg_free, j & 1);  // the drain has read the factor columns out of the dP^T region
+          tc_fence_after();
+          issue_dq(j);
+        } else {
+          issue_dq(j);
+          issue_dk(j);
+          if constexpr (MC) tc_commit_mc(&bars->q_empty[j & 1], kPair);
+          else tc_commit(&bars->q_empty[j & 1]);
+        }
         tc_commit(&bars->ds_free);
       };
       mbar_wait(&bars->res_full, 0);
@@ -446,8 +492,45 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const bool leader = dd == 0;
     int chunk = 0;
+    constexpr int QC = T128_QCHUNK, RB = QC * 4, NST = 16384 / (128 * RB);  // row bytes, stages
+    float duk[LEARN ? 16 : 1];
+#pragma unroll
+    for (int c = 0; c < (LEARN ? 16 : 1); ++c) duk[c] = 0.f;
     for (int j = 0; j < nblk; ++j) {
       const int q0 = (i_start + j) * 128;
+      // MC odd tile, causal: the first shared block lies entirely above this tile's diagonal (dQ^T = 0)
+      const bool skip = MC && p.causal && q0 + 128 <= kv0;
+      if constexpr (LEARN) {
+        static_assert(!LEARN || RB == 64, "the dUq chunk reuses the 64-byte-row stage geometry");
+        mbar_wait(&bars->fg_full, j & 1);
+        tc_fence_after();
+        uint32_t f[32];  // [0,16): dUk part (lane = key), [16,32): dUq (lane = query)
+        tmem_ld32(tmem + lane_off + T_DP, f);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars->fg_free);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) duk[c] += __uint_as_float(f[c]);
+        if (!skip) {  // the 128 x 16 dUq block: one more 8 KB chunk through the dQ stages
+          uint8_t* stg = reinterpret_cast<uint8_t*>(dq_stage) + (chunk % NST) * (128 * RB);
+          if (leader) t128_wait_read<NST - 1>();
+          named_bar_sync(3, 128);
+          const float sc = p.scale;
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4)
+            *reinterpret_cast<float4*>(stg + dd * RB + ((c4 ^ ((dd * RB >> 7) & (RB / 16 - 1))) << 4)) =
+                make_float4(__uint_as_float(f[16 + 4 * c4]) * sc, __uint_as_float(f[17 + 4 * c4]) * sc,
+                            __uint_as_float(f[18 + 4 * c4]) * sc, __uint_as_float(f[19 + 4 * c4]) * sc);
+          fence_proxy_async();
+          named_bar_sync(3, 128);
+          if (leader) {
+            t128_reduce_add(&tm_duq, stg, 0, q0, h, b);
+            t128_bulk_commit();
+          }
+          ++chunk;
+        }
+      }
       mbar_wait(&bars->dq_full, j & 1);
       tc_fence_after();
       if (leader) trace(p.trace, p.trace_cta, 19, j);
@@ -459,9 +542,6 @@ __global__ void __launch_bounds__(512, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars->dq_free);
-      constexpr int QC = T128_QCHUNK, RB = QC * 4, NST = 16384 / (128 * RB);  // row bytes, stages
-      // MC odd tile, causal: the first shared block lies entirely above this tile's diagonal (dQ^T = 0)
-      const bool skip = MC && p.causal && q0 + 128 <= kv0;
 #pragma unroll
       for (int c = 0; c < (skip ? 0 : 128 / QC); ++c, ++chunk) {
         uint8_t* stg = reinterpret_cast<uint8_t*>(dq_stage) + (chunk % NST) * (128 * RB);
@@ -490,6 +570,17 @@ __global__ void __launch_bounds__(512, 1)
       if (leader) trace(p.trace, p.trace_cta, 20, j);
     }
     if (leader) t128_wait_all();
+    if constexpr (LEARN) {  // dUk rows (lane dd = key kv0 + dd), fp32, scaled like dK
+      const int kv = kv0 + dd;
+      if (kv < p.M) {
+        float* dst = p.duk + static_cast<int64_t>(b) * p.duk_sb + static_cast<int64_t>(h) * p.duk_sh +
+                     static_cast<int64_t>(kv) * p.duk_sn;
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4)
+          reinterpret_cast<float4*>(dst)[c4] = make_float4(duk[4 * c4] * p.scale, duk[4 * c4 + 1] * p.scale,
+                                                           duk[4 * c4 + 2] * p.scale, duk[4 * c4 + 3] * p.scale);
+      }
+    }
   }
 
   tc_fence_before();
@@ -506,10 +597,11 @@ __global__ void __launch_bounds__(512, 1)
 #define T128_MULTICAST 1
 #endif
 
-template <int RP, bool BF16, bool MC>
-static cudaError_t launch_t128_mc(const BwdMaps& m, const CUtensorMap& dqacc, const BwdParams& p, cudaStream_t s) {
+template <int RP, bool BF16, bool MC, bool LEARN>
+static cudaError_t launch_t128_mc(const BwdMaps& m, const CUtensorMap& dqacc, const CUtensorMap& duq,
+                                  const BwdParams& p, cudaStream_t s) {
   using Cfg = T128Cfg<RP>;
-  auto k = fb_bwd_t128_kernel<RP, BF16, MC>;
+  auto k = fb_bwd_t128_kernel<RP, BF16, MC, LEARN>;
   static std::atomic<uint64_t> attr_mask{0};
   cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(k), Cfg::kSmem);
   if (e != cudaSuccess) return e;
@@ -525,16 +617,17 @@ static cudaError_t launch_t128_mc(const BwdMaps& m, const CUtensorMap& dqacc, co
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, k, m.q128, m.do128, m.uq128, m.k128, m.v128, m.uk128, dqacc, p);
+  e = cudaLaunchKernelEx(&cfg, k, m.q128, m.do128, m.uq128, m.k128, m.v128, m.uk128, dqacc, duq, p);
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 // cluster pairs need an even number of key tiles per head (adjacent tiles of one head)
-template <int RP, bool BF16>
-static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, const BwdParams& p, cudaStream_t s) {
+template <int RP, bool BF16, bool LEARN>
+static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, const CUtensorMap& duq,
+                                 const BwdParams& p, cudaStream_t s) {
   const int nkt = (p.M + 127) / 128;
-  if (T128_MULTICAST && nkt % 2 == 0) return launch_t128_mc<RP, BF16, true>(m, dqacc, p, s);
-  return launch_t128_mc<RP, BF16, false>(m, dqacc, p, s);
+  if (T128_MULTICAST && nkt % 2 == 0) return launch_t128_mc<RP, BF16, true, LEARN>(m, dqacc, duq, p, s);
+  return launch_t128_mc<RP, BF16, false, LEARN>(m, dqacc, duq, p, s);
 }
 
 // dq[b,h,n,:] = acc_t[b,h,:,n]: 64-query x 128-dim tiles transposed through
@@ -587,13 +680,19 @@ int bwd_t128_qchunk() { return T128_QCHUNK; }
 int bwd_t128_box_rows() { return 128; }
 
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads) {
-  return d == 128 && rp <= 1 && !dense && !factor_grads;
+  return d == 128 && !dense && (factor_grads ? rp == 1 : rp <= 1);
 }
 
-cudaError_t launch_bwd_t128_sm100(int rp, bool bf16, const BwdMaps& m, const CUtensorMap& dqacc,
-                                  const BwdParams& p, cudaStream_t s) {
-  if (rp == 0) return bf16 ? launch_t128_t<0, true>(m, dqacc, p, s) : launch_t128_t<0, false>(m, dqacc, p, s);
-  if (rp == 1) return bf16 ? launch_t128_t<1, true>(m, dqacc, p, s) : launch_t128_t<1, false>(m, dqacc, p, s);
+cudaError_t launch_bwd_t128_sm100(int rp, bool bf16, bool fgrad, const BwdMaps& m, const CUtensorMap& dqacc,
+                                  const CUtensorMap& duq, const BwdParams& p, cudaStream_t s) {
+  if (fgrad) {
+    if (rp != 1) return cudaErrorInvalidValue;
+    return bf16 ? launch_t128_t<1, true, true>(m, dqacc, duq, p, s) : launch_t128_t<1, false, true>(m, dqacc, duq, p, s);
+  }
+  if (rp == 0)
+    return bf16 ? launch_t128_t<0, true, false>(m, dqacc, duq, p, s) : launch_t128_t<0, false, false>(m, dqacc, duq, p, s);
+  if (rp == 1)
+    return bf16 ? launch_t128_t<1, true, false>(m, dqacc, duq, p, s) : launch_t128_t<1, false, false>(m, dqacc, duq, p, s);
   return cudaErrorInvalidValue;
 }
 

@@ -431,7 +431,13 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
   // FB_BWD_DETERMINISTIC (or the FB_FORCE_SPLIT_BWD=1 testing hook, read once) selects the two-kernel
   // backward: no atomics, every gradient element written once in a fixed order
   const bool deterministic = force_split || (flags & FB_BWD_DETERMINISTIC);
-  const bool fused = !deterministic && ((D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
+  static const int t128_off = [] {
+    const char* v = getenv("FB_BWD_T128");
+    return v && v[0] == '0' ? 1 : 0;
+  }();
+  // learnable factors at d = 128 ride the 128x128-tile kernel when they fit one 16-column panel
+  const bool use_t128 = !t128_off && bwd_t128_supported(D, rp, bias != nullptr, duq != nullptr);
+  const bool fused = !deterministic && (use_t128 || (D == 128 && duq == nullptr) || (D == 64 && rp <= 4));
   if (dbias && !fused)
     return fail(FB_ECONFIG, "the dense-bias gradient is produced by the fused backward (head dim 64/128, "
                             "not deterministic)");
@@ -445,11 +451,7 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
     tacc.dtype = FB_F32;
     CUtensorMap macc;
     if ((rc = make_map(&macc, &tacc, D, 32, 0, "dq_acc"))) return rc;
-    static const int t128_off = [] {
-      const char* v = getenv("FB_BWD_T128");
-      return v && v[0] == '0' ? 1 : 0;
-    }();
-    if (!t128_off && bwd_t128_supported(D, rp, bias != nullptr, duq != nullptr)) {
+    if (use_t128) {
       // transposed accumulator [B,H,D,N4]: qchunk-query x 128-dim boxes, swizzled to the row width
       const int64_t n4 = ((int64_t)N + 3) / 4 * 4;
       fb_tensor tt{};
@@ -463,7 +465,21 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
       if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
       p.dq_acc = acc;
       p.acc_n4 = (int)n4;
-      e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, maps, macc_t, p, s);
+      CUtensorMap mduq;
+      memset(&mduq, 0, sizeof(mduq));
+      if (duq) {  // dUq is reduce-added in 128-query x 16-column boxes: start from zero
+        if (duq->stride[3] != 1 || duq->shape[3] != 16 || duk->stride[3] != 1 || duk->shape[3] != 16 ||
+            (duk->stride[2] * 4) % 16)
+          return fail(FB_ESHAPE, "factor gradient outputs must be [B,H,L,16] fp32 with contiguous 16-byte rows");
+        if ((rc = make_map(&mduq, duq, 16, 128, 64, "duq"))) return rc;
+        for (int64_t bb = 0; bb < duq->shape[0]; ++bb)
+          for (int64_t hh = 0; hh < duq->shape[1]; ++hh) {
+            e = cudaMemsetAsync(static_cast<float*>(duq->data) + bb * duq->stride[0] + hh * duq->stride[1], 0,
+                                (size_t)duq->shape[2] * duq->stride[2] * sizeof(float), s);
+            if (e != cudaSuccess) return cuda_fail(e, "memset duq");
+          }
+      }
+      e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, duq != nullptr, maps, macc_t, mduq, p, s);
       if (e != cudaSuccess) return cuda_fail(e, "bwd_t128_sm100");
       e = launch_dq_convert_t(acc, (int)n4, p, q->dtype == FB_BF16, s);
       note_launch(2);

@@ -104,12 +104,15 @@ cudaError_t launch_bwd_sm100(int d, int rp, bool dense, bool bf16, bool factor_g
 // an fp32 accumulator [B,H,N,128] through TMA bulk reductions, then converted
 cudaError_t launch_bwd_fused_sm100(int rp, bool dense, bool bf16, const BwdMaps& maps, const CUtensorMap& dqacc,
                                    const BwdParams& p, cudaStream_t s);
-// d = 128 on 128-key x 128-query tiles (every GEMM N = 128), Rpad <= 16, no dense bias / factor grads
+// d = 128 on 128-key x 128-query tiles (every GEMM N = 128), Rpad <= 16 (factor gradients: Rpad == 16), no
+// dense bias
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads);
 int bwd_t128_qchunk();
 int bwd_t128_box_rows();  // head-dim rows per dQ reduce box (128, or 32 for per-warp boxes)  // queries per dQ reduce box (transposed accumulator map: box {qchunk, 128}, swizzle qchunk*4 B)
-cudaError_t launch_bwd_t128_sm100(int rp, bool bf16, const BwdMaps& maps, const CUtensorMap& dqacc,
-                                  const BwdParams& p, cudaStream_t s);
+// fgrad: dUq reduce-added through `duq` (fp32 [B,H,N,16], box {16, 128}, 64-byte swizzle, zeroed by the
+// caller), dUk written to p.duk
+cudaError_t launch_bwd_t128_sm100(int rp, bool bf16, bool fgrad, const BwdMaps& maps, const CUtensorMap& dqacc,
+                                  const CUtensorMap& duq, const BwdParams& p, cudaStream_t s);
 // dq[b,h,n,:] = acc_t[b,h,:,n] (transposed fp32 accumulator [B,H,128,n4] of the 128x128-tile kernel)
 cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_dq_convert(const float* acc, int d, const BwdParams& p, bool bf16, cudaStream_t s);

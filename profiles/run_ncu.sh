@@ -18,4 +18,9 @@ for K in fb_fwd_kernel "fb_bwd_(t128|fused|fused64|dkv)_kernel"; do
   NAME=$( [ "$K" = fb_fwd_kernel ] && echo fwd || echo bwd )
   ncu --profile-from-start off --set full --clock-control none --import-source on -k "regex:${K}" -s 1 -c 1 \
       -o gpurun_out/prof_${TAG}_${CFG}_${NAME} -f python bench.py $ARGS > /dev/null 2>&1 || true
+  # gpurun copies back <= 64 MiB: keep the raw-page CSV (what summarize.py reads), drop the report unless asked
+  if [ -f gpurun_out/prof_${TAG}_${CFG}_${NAME}.ncu-rep ]; then
+    ncu -i gpurun_out/prof_${TAG}_${CFG}_${NAME}.ncu-rep --page raw --csv > gpurun_out/prof_${TAG}_${CFG}_${NAME}.raw.csv
+    [ -n "${KEEP_REP:-}" ] || rm -f gpurun_out/prof_${TAG}_${CFG}_${NAME}.ncu-rep
+  fi
 done

@@ -48,7 +48,10 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns
 
 
 def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # exported on the GPU box by run_ncu.sh
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, vals = rows[0], rows[1], rows[2]
     return {h: (v, u) for h, u, v in zip(hdr, units, vals)}
@@ -68,8 +71,12 @@ def main(tag, cfg):
              f"bench.py workload {cfg}, one launch per kernel after warm-up. "
              "ncu replays each kernel ~40x with cold caches: compare shares/ratios, not absolute times.", ""]
     traffic = {}
-    for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_{cfg}_*.ncu-rep"))):
-        name = os.path.basename(rep)[len(f"prof_{tag}_{cfg}_"):-len(".ncu-rep")]
+    reps = {}
+    for rep in sorted(glob.glob(os.path.join(OUT, f"prof_{tag}_{cfg}_*.ncu-rep")) +
+                      glob.glob(os.path.join(OUT, f"prof_{tag}_{cfg}_*.raw.csv"))):
+        name = os.path.basename(rep)[len(f"prof_{tag}_{cfg}_"):].split(".")[0]
+        reps.setdefault(name, rep)
+    for name, rep in sorted(reps.items()):
         m = raw(rep)
         lines += [f"## {name}", "", "| metric | value |", "|---|---|"]
         got = {}

@@ -225,3 +225,93 @@ def test_bwd_fp16_static(D, R, causal):
     for name, got, r_ in zip(["dq", "dk", "dv"], (q.grad, k.grad, v.grad), ref_leaves):
         e = relerr(got, r_.grad)
         assert e < BF16_TOL, f"{name}: rel err {e:.3e}"
+
+
+def _bwd_learn_case(B, H, N, M, R, causal, seed=0, factor_batch=1, dtype=torch.bfloat16, alibi=False):
+    """Learnable factors at d=128 with one 16-column panel: the 128x128-tile backward's LEARN variant
+    (dUk / dUq as extra N=16 MMAs, fb_bwd_t128_sm100.cu); every gradient against torch fp64 autograd."""
+    q, k, v = _qkv(B, H, N, M, 128, dtype, seed=seed)
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    g = torch.Generator(device="cuda").manual_seed(seed + 13)
+    if alibi:  # ALiBi-shaped factors (3-way split of large-magnitude columns) with learnable slopes
+        slopes = torch.tensor([-(2.0 ** (-8.0 * (i + 1) / H)) for i in range(H)], device="cuda")
+        fq0, fk0 = fb.alibi_factors(slopes.tolist(), N, M)
+        fq, fk = fq0.clone().float(), fk0.clone().float()
+    else:
+        fq = torch.randn(factor_batch, H, N, R, device="cuda", generator=g) * 0.6
+        fk = torch.randn(factor_batch, H, M, R, device="cuda", generator=g) * 0.6
+    fq.requires_grad_(True)
+    fk.requires_grad_(True)
+    do = torch.randn(B, H, N, 128, device="cuda", generator=g).to(dtype)
+    mask = "causal" if causal else "none"
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask=mask)
+    out.backward(do)
+    leaves = [q, k, v, fq, fk]
+    ref_leaves = [t.detach().double().requires_grad_(True) for t in leaves]
+    ref = ref_attention(*ref_leaves, causal=causal)
+    ref.backward(do.double())
+    for name, t, r_ in zip(["dq", "dk", "dv", "dfq", "dfk"], leaves, ref_leaves):
+        e = relerr(t.grad, r_.grad)
+        assert e < BF16_TOL, f"{name}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("B,H,N,M,R,causal,fb_", [
+    (2, 2, 384, 384, 2, True, 1),      # odd key-tile count: single-CTA variant; batch-broadcast factors
+    (1, 2, 512, 512, 2, True, 1),      # even key-tile count: cluster-multicast variant, causal
+    (2, 2, 512, 512, 4, False, 2),     # multicast, non-causal, per-batch factors
+    (1, 2, 200, 200, 3, True, 1),      # ragged causal
+    (1, 1, 150, 333, 5, False, 1),     # N != M, ragged both sides
+])
+def test_bwd_t128_learnable_factors(B, H, N, M, R, causal, fb_):
+    plan = A.plan_factor_fold(torch.randn(1, 1, 8, R, device="cuda") * 0.6,
+                              torch.randn(1, 1, 8, R, device="cuda") * 0.6, 1 / math.sqrt(128))
+    assert R * plan.split * (plan.split + 1) // 2 <= 16  # one panel: the LEARN 128x128-tile kernel
+    _bwd_learn_case(B, H, N, M, R, causal, seed=N + R, factor_batch=fb_)
+
+
+def test_bwd_t128_learnable_alibi_slopes():
+    """C3-shaped learnable ALiBi (rank 2, 3-way split into 12 columns) at N=2048, causal, 4 heads.
+
+    dq/dk/dv at 2e-2 against fp64 autograd.  The factor gradient dfq = dS @ fk is a
+    cancelling sum here (rows of dS sum to zero while fk grows linearly with the key
+    index), so the kernel's bf16 dS operand bounds its accuracy, not the kernel:
+    dfq/dfk are checked against the exact value at 2e-2 of the summand magnitude
+    sum_j |dS_ij| |fk_j| (a bf16 dS element carries 2^-8 of its own size, so this
+    is the scale its rounding error lives on)."""
+    B, H, N = 1, 4, 2048
+    q, k, v = _qkv(B, H, N, N, 128, torch.bfloat16, seed=7)
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    slopes = [-(2.0 ** (-8.0 * (i + 1) / H)) for i in range(H)]
+    fq0, fk0 = fb.alibi_factors(slopes, N, N)
+    fq, fk = fq0.clone().float().requires_grad_(True), fk0.clone().float().requires_grad_(True)
+    do = torch.randn(B, H, N, 128, device="cuda", generator=torch.Generator(device="cuda").manual_seed(3)).bfloat16()
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask="causal")
+    out.backward(do)
+    leaves = [q, k, v, fq, fk]
+    ref_leaves = [t.detach().double().requires_grad_(True) for t in leaves]
+    ref = ref_attention(*ref_leaves, causal=True)
+    ref.backward(do.double())
+    for name, t, r_ in zip(["dq", "dk", "dv"], leaves[:3], ref_leaves[:3]):
+        e = relerr(t.grad, r_.grad)
+        assert e < BF16_TOL, f"{name}: rel err {e:.3e}"
+    with torch.no_grad():  # dS in fp64 from the reference forward, then the kernel's bf16 rounding of it
+        qd, kd, vd, fqd, fkd, dod = (x.double() for x in (q, k, v, fq, fk, do))
+        s = qd @ kd.transpose(-1, -2) / math.sqrt(128) + fqd @ fkd.transpose(-1, -2)
+        s = s.masked_fill(torch.ones(N, N, dtype=torch.bool, device="cuda").triu(1), float("-inf"))
+        p = torch.softmax(s, -1)
+        dp = dod @ vd.transpose(-1, -2)
+        ds = p * (dp - (dp * p).sum(-1, keepdim=True))
+        scale_of = {"dfq": ds.abs() @ fkd.abs(), "dfk": ds.abs().transpose(-1, -2) @ fqd.abs()}
+        exact = {"dfq": ref_leaves[3].grad, "dfk": ref_leaves[4].grad}
+    for name, t in (("dfq", fq), ("dfk", fk)):
+        got = t.grad.double()
+        # rows whose dS is exactly 0 in fp64 (the first causal row) get the tensor's summand scale
+        m = scale_of[name]
+        e2 = float(((got - exact[name]).abs() / (m + 1e-3 * m.amax())).max())
+        assert e2 < BF16_TOL, f"{name}: err {e2:.3e} relative to sum |dS| |f|"
+
+
+def test_bwd_t128_learnable_fp16():
+    _bwd_learn_case(1, 2, 256, 256, 2, True, seed=9, dtype=torch.float16)
