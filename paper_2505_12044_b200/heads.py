@@ -111,6 +111,18 @@ def split_heads_by_rank(biases: Sequence, energy_threshold: float, max_rank: int
     return HeadSplit(low, factors, dense, common, low_fq=fq, low_fk=fk)
 
 
+_SIDE = {}
+
+
+def _side_stream(device):
+    """One cached side stream per device for the concurrent subset launch."""
+    import torch
+    key = torch.device(device).index
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
 def mixed_head_attention(q, k, v, split: HeadSplit, biases, mask: str = MASK_NONE,
                          tiles: Optional[TileConfig] = None, *, precision: Optional[str] = None):
     """Per-head attention with the split's factored heads on the FlashBias
@@ -153,14 +165,23 @@ def mixed_head_attention(q, k, v, split: HeadSplit, biases, mask: str = MASK_NON
         return t.index_select(dim, torch.tensor(idx, device=t.device))
 
     parts = []
+    # Both subsets at once: each launch alone under-fills the 148 SMs at small head counts, so the
+    # FlashBias launch runs on a side stream next to the dense-bias launch (autograd runs each
+    # backward on its forward's stream, so the backwards overlap too).
+    both = bool(split.low_indices) and bool(split.dense_indices)
+    cur = torch.cuda.current_stream(qh.device)
+    side = _side_stream(qh.device) if both else cur
+    if both:
+        side.wait_stream(cur)
     if split.low_indices:
         li = split.low_indices
         fq = split.low_fq if split.low_fq is not None else torch.stack([torch.as_tensor(f.fq) for f in split.low_factors])
         fk = split.low_fk if split.low_fk is not None else torch.stack([torch.as_tensor(f.fk) for f in split.low_factors])
         # the low subset: one FlashBias launch over the [1, H_low, ...] stack
-        o_low = flashbias_attention(take(qh, li), take(kh, li), take(vh, li),
-                                    fq.to("cuda").unsqueeze(0), fk.to("cuda").unsqueeze(0), mask=mask,
-                                    tiles=tiles, precision=precision)
+        with torch.cuda.stream(side):
+            o_low = flashbias_attention(take(qh, li), take(kh, li), take(vh, li),
+                                        fq.to("cuda").unsqueeze(0), fk.to("cuda").unsqueeze(0), mask=mask,
+                                        tiles=tiles, precision=precision)
         parts.append((li, o_low))
     if split.dense_indices:
         di = split.dense_indices
@@ -168,6 +189,9 @@ def mixed_head_attention(q, k, v, split: HeadSplit, biases, mask: str = MASK_NON
         o_dense = tiled_attention(take(qh, di), take(kh, di), take(vh, di),
                                   DenseBias(take(b, di, 0).unsqueeze(0)), mask=mask, tiles=tiles, precision=precision)
         parts.append((di, o_dense))
+    if both:
+        cur.wait_stream(side)
+        o_low.record_stream(cur)
     if len(parts) == 2 and parts[0][0] + parts[1][0] == list(range(nh)):
         out = torch.cat([parts[0][1], parts[1][1]], 1)
     elif len(parts) == 2 and parts[1][0] + parts[0][0] == list(range(nh)):
