@@ -358,6 +358,28 @@ def prepare_factor_panels_cached(fq, fk, premul: float, split: int, dtype):
     return panels
 
 
+_F32_CACHE: dict = {}
+
+
+def _fp32_factors_cached(fq, fk, scale: float):
+    """The fp32 path's factor operands uq = fq / scale, uk = fk (fp32, contiguous), memoised like
+    prepare_factor_panels_cached so static factors cost no per-call elementwise launch."""
+    import weakref
+    bq, bk = _base_of(fq), _base_of(fk)
+
+    def geom(t, base):
+        return (id(base), base._version, t.storage_offset(), tuple(t.shape), tuple(t.stride()), t.dtype, t.device)
+    key = (geom(fq, bq), geom(fk, bk), float(scale))
+    hit = _F32_CACHE.get(key)
+    if hit is not None and hit[0]() is bq and hit[1]() is bk:
+        return hit[2]
+    ops = ((fq.float() / scale).contiguous(), fk.float().contiguous())
+    if len(_F32_CACHE) >= 8:
+        _F32_CACHE.pop(next(iter(_F32_CACHE)))
+    _F32_CACHE[key] = (weakref.ref(bq), weakref.ref(bk), ops)
+    return ops
+
+
 def fold_factor_grads(dpanel, like, side: int, split: int, postmul: float):
     """fb_fold_factor_grads: split-panel gradients -> logical factor gradient shaped like ``like``."""
     import torch
@@ -523,8 +545,7 @@ def _attention_on_device(q, k, v, fq, fk, bias, mask, scale, cdt, split, shp, de
         qf, kf, vf = (t.contiguous() for t in (qt, kt, vt))
         uq = uk = None
         if fqt is not None:
-            uq = (fqt.float() / scale).contiguous()
-            uk = fkt.float().contiguous()
+            uq, uk = _fp32_factors_cached(fqt, fkt, scale)
         bf = bt.float().contiguous() if bt is not None else None
         o, _ = _fwd_launch(qf, kf, vf, uq, uk, bf, mask_code, scale, need_lse=False)
     else:

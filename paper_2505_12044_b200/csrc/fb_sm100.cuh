@@ -66,6 +66,12 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+#ifndef FB_MBAR_TIMEOUT_LOG2
+#define FB_MBAR_TIMEOUT_LOG2 34
+#endif
+#ifndef FB_MBAR_NOTRAP
+#define FB_MBAR_NOTRAP 0
+#endif
 // Wait for the phase with the given parity to complete.  A bounded spin:
 // a protocol bug traps after ~2^33 cycles instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -73,10 +79,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(a, parity)) return;
   long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
-    if (clock64() - t0 > (1ll << 34)) {
+    if (clock64() - t0 > (1ll << FB_MBAR_TIMEOUT_LOG2)) {
       printf("flashbias: mbarrier timeout block %d thread %d bar %u parity %u\n", blockIdx.x,
              threadIdx.x, a, parity);
+#if FB_MBAR_NOTRAP  // debug builds only: report every stuck role, then fall through
+      return;
+#else
       __trap();
+#endif
+    }
+  }
+}
+
+// The same bounded wait without the printf: a vprintf call site forces every value live across it
+// into local memory, so waits placed while a thread holds a large register array use this one.
+__device__ __forceinline__ void mbar_wait_nocall(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << FB_MBAR_TIMEOUT_LOG2)) {
+#if FB_MBAR_NOTRAP
+      return;
+#else
+      __trap();
+#endif
     }
   }
 }

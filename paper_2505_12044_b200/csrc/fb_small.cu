@@ -535,30 +535,47 @@ __global__ void __launch_bounds__(128) fwd_simt_f32_kernel(const SimtParams p) {
   }
 }
 
+// 16-byte global -> shared copies that bypass registers (cp.async, Ampere+); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Register-tiled SIMT forward (same numerics as fwd_simt_f32_kernel: fp32 FMA
-// q.k, fp64 factor / bias terms and running max, expf of the fp32 difference):
-// CTA = BM query rows x 256 threads (16 x 16), KV blocks of 64 keys; thread
-// (ty, tx) owns rows RT*ty.. x keys 4tx..4tx+3 of S and rows RT*ty.. x head
-// columns CPT*tx.. of O.  Q^T / K^T tiles are stored channel-major in shared
-// memory so every channel step is two vector loads feeding 4*RT FMAs; P goes
-// through shared memory to the P.V product.
+// q.k in channel order, fp64 factor / bias terms and running max, expf of the
+// fp32 difference): CTA = BM query rows x 256 threads (16 x 16), KV blocks of
+// 64 keys.  Thread (ty, tx) owns query rows ty + 16i and keys tx + 16kk of S
+// and rows ty + 16i x head columns CPT*tx.. of O.  Q, K, V tiles are row-major
+// in shared memory with a 4-float pad (rows D + 4 apart): the eight threads of
+// a quarter-warp read eight different rows' float4 at conflict-free banks, and
+// every 4 channels cost 8 LDS.128 for 64 FMAs.  Tiles arrive by cp.async,
+// software-pipelined: K(j+1) is in flight during softmax(j) and P.V(j), V(j+1)
+// during Q.K(j+1) and softmax(j+1).  The factor columns live in fp64 (converted
+// once per load), so the softmax step forms the factor term without per-use
+// conversions; at <= 80 registers three CTAs share an SM.
 //
 // Split-KV over a thread-block cluster (SPLIT CTAs, one per KV range of the
 // same row block): small grids (C1: 8 heads x 1024 rows) otherwise leave most
 // SMs idle while each CTA walks every KV block serially.  Each CTA keeps its
-// partial (m, l, acc) in shared memory; after a cluster barrier the rank-0 CTA
-// reads the peers' partials over DSMEM and combines them -- no global scratch,
-// one launch.
+// partial (m, l, acc) in shared memory; after a cluster barrier every rank
+// combines BM / SPLIT of the rows from all partials over DSMEM and writes them
+// -- no global scratch, one launch, no serial combine tail.
 template <int D, int BM, int SPLIT>
-__global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p) {
-  constexpr int BN = 64, CPT = D / 16, RT = BM / 16;  // rows per thread
-  extern __shared__ float sm[];
-  const int R = p.R, DK = D + R;
-  float* sQ = sm;                  // [DK][BM]
-  float* sK = sQ + DK * BM;        // [DK][BN]
-  float* sV = sK + DK * BN;        // [BN][D]
-  float* sP = sV + BN * D;         // [BM][BN + 4]
-  constexpr int PST = BN + 4;
+__global__ void __launch_bounds__(256, D <= 64 ? 3 : 1) fwd_simt_tiled_kernel(const SimtParams p) {
+  constexpr int BN = 64, CPT = D / 16, RT = BM / 16, KB = BN / 16;  // rows, keys per thread
+  constexpr int TS = D + 4, PST = BN + 8, C4 = D / 4;
+  extern __shared__ __align__(16) float sm[];
+  const int R = p.R;
+  float* sQ = sm;                  // [BM][TS]
+  float* sK = sQ + BM * TS;        // [BN][TS]
+  float* sV = sK + BN * TS;        // [BN][D]
+  float* sP = sV + BN * D;         // [BM][PST]
+  double* sQf = reinterpret_cast<double*>(sP + BM * PST);  // [R][BM]
+  double* sKf = sQf + R * BM;                               // [2][R][BN] (double-buffered)
   const int b = blockIdx.z, h = blockIdx.y;
   const int rank = SPLIT > 1 ? static_cast<int>(blockIdx.x % SPLIT) : 0;
   const int q0 = (blockIdx.x / SPLIT) * BM;
@@ -566,21 +583,56 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
   const float* qb = p.q + b * p.q_sb + h * p.q_sh;
   const float* kb = p.k + b * p.k_sb + h * p.k_sh;
   const float* vb = p.v + b * p.v_sb + h * p.v_sh;
-  // q rows: D / 4 float4 per row (compile-time index math), then the R factor columns
-  for (int idx = t; idx < BM * (D / 4); idx += 256) {
-    const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4, row = q0 + r;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (row < p.N) v = *reinterpret_cast<const float4*>(qb + static_cast<int64_t>(row) * p.q_sn + c4);
-    sQ[(c4 + 0) * BM + r] = v.x;
-    sQ[(c4 + 1) * BM + r] = v.y;
-    sQ[(c4 + 2) * BM + r] = v.z;
-    sQ[(c4 + 3) * BM + r] = v.w;
+  const float* ukb = R > 0 ? p.uk + b * p.uk_sb + h * p.uk_sh : nullptr;
+
+  const int kv_all = p.causal ? min(p.M, q0 + BM) : p.M;
+  const int nkv = (kv_all + BN - 1) / BN;
+  const int kb0 = nkv * rank / SPLIT, kb1 = nkv * (rank + 1) / SPLIT;  // this CTA's KV blocks
+  auto load_k = [&](int kblk) {
+    const int kv0 = kblk * BN;
+#pragma unroll
+    for (int it = 0; it < BN * C4 / 256; ++it) {
+      const int idx = t + 256 * it, r = idx / C4, c4 = (idx % C4) * 4, j = kv0 + r;
+      cp_async16(sK + r * TS + c4, kb + static_cast<int64_t>(j < p.M ? j : 0) * p.k_sn + c4, j < p.M);
+    }
+  };
+  auto load_v = [&](int kblk) {
+    const int kv0 = kblk * BN;
+#pragma unroll
+    for (int it = 0; it < BN * C4 / 256; ++it) {
+      const int idx = t + 256 * it, r = idx / C4, c4 = (idx % C4) * 4, j = kv0 + r;
+      cp_async16(sV + r * D + c4, vb + static_cast<int64_t>(j < p.M ? j : 0) * p.v_sn + c4, j < p.M);
+    }
+  };
+  auto load_kf = [&](int kblk) {  // the R key-factor columns of a block, fp64, into buffer kblk & 1
+    const int kv0 = kblk * BN;
+    double* dst = sKf + (kblk & 1) * R * BN;
+    for (int idx = t; idx < BN * R; idx += 256) {
+      const int r = idx % BN, c = idx / BN, j = kv0 + r;
+      dst[c * BN + r] = j < p.M ? static_cast<double>(ukb[static_cast<int64_t>(j) * p.uk_sn + c]) : 0.0;
+    }
+  };
+  // prologue: Q and the first K / V block
+#pragma unroll
+  for (int it = 0; it < BM * C4 / 256; ++it) {
+    const int idx = t + 256 * it, r = idx / C4, c4 = (idx % C4) * 4, row = q0 + r;
+    cp_async16(sQ + r * TS + c4, qb + static_cast<int64_t>(row < p.N ? row : 0) * p.q_sn + c4, row < p.N);
   }
+  if (kb0 < kb1) {
+    load_k(kb0);
+    load_v(kb0);
+  }
+  cp_async_commit();
   for (int idx = t; idx < BM * R; idx += 256) {
-    const int r = idx / R, c = idx % R, row = q0 + r;
-    sQ[(D + c) * BM + r] =
-        row < p.N ? p.uq[b * p.uq_sb + h * p.uq_sh + static_cast<int64_t>(row) * p.uq_sn + c] : 0.f;
+    const int r = idx % BM, c = idx / BM, row = q0 + r;
+    sQf[c * BM + r] =
+        row < p.N ? static_cast<double>(p.uq[b * p.uq_sb + h * p.uq_sh + static_cast<int64_t>(row) * p.uq_sn + c])
+                  : 0.0;
   }
+  if (kb0 < kb1) load_kf(kb0);
+  cp_async_wait<0>();
+  __syncthreads();
+
   double m_run[RT];
   float l_run[RT], acc[RT][CPT];
 #pragma unroll
@@ -590,94 +642,73 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[i][c] = 0.f;
   }
-  const int kv_all = p.causal ? min(p.M, q0 + BM) : p.M;
-  const int nkv = (kv_all + BN - 1) / BN;
-  const int kb0 = nkv * rank / SPLIT, kb1 = nkv * (rank + 1) / SPLIT;  // this CTA's KV blocks
   for (int kblk = kb0; kblk < kb1; ++kblk) {
     const int kv0 = kblk * BN;
-    __syncthreads();  // previous block's sK / sV / sP fully consumed
-    for (int idx = t; idx < BN * (D / 4); idx += 256) {
-      const int r = idx / (D / 4), c4 = (idx % (D / 4)) * 4, j = kv0 + r;
-      float4 kv = make_float4(0.f, 0.f, 0.f, 0.f), vv = kv;
-      if (j < p.M) {
-        kv = *reinterpret_cast<const float4*>(kb + static_cast<int64_t>(j) * p.k_sn + c4);
-        vv = *reinterpret_cast<const float4*>(vb + static_cast<int64_t>(j) * p.v_sn + c4);
-      }
-      sK[(c4 + 0) * BN + r] = kv.x;
-      sK[(c4 + 1) * BN + r] = kv.y;
-      sK[(c4 + 2) * BN + r] = kv.z;
-      sK[(c4 + 3) * BN + r] = kv.w;
-      *reinterpret_cast<float4*>(sV + r * D + c4) = vv;
-    }
-    for (int idx = t; idx < BN * R; idx += 256) {
-      const int r = idx / R, c = idx % R, j = kv0 + r;
-      sK[(D + c) * BN + r] = j < p.M ? p.uk[b * p.uk_sb + h * p.uk_sh + static_cast<int64_t>(j) * p.uk_sn + c] : 0.f;
-    }
-    __syncthreads();
-    float s[RT][4];
+    const bool more = kblk + 1 < kb1;
+    // interior blocks (no key padding, no causal diagonal, no bias rows past N) skip the per-element masks
+    const bool edge = kv0 + BN > p.M || (p.causal && kv0 + BN - 1 > q0) || q0 + BM > p.N;
+    float s[RT][KB];
 #pragma unroll
     for (int i = 0; i < RT; ++i)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) s[i][k] = 0.f;
-    auto qrow = [&](int c, float (&av)[RT]) {
-      if constexpr (RT == 4) {
-        const float4 a = *reinterpret_cast<const float4*>(sQ + c * BM + RT * ty);
-        av[0] = a.x; av[1] = a.y; av[2] = a.z; av[3] = a.w;
-      } else {
-        const float2 a = *reinterpret_cast<const float2*>(sQ + c * BM + RT * ty);
-        av[0] = a.x; av[1] = a.y;
-      }
-    };
-#pragma unroll 8
-    for (int c = 0; c < D; ++c) {
-      float av[RT];
-      qrow(c, av);
-      const float4 kk = *reinterpret_cast<const float4*>(sK + c * BN + 4 * tx);
-      const float kv[4] = {kk.x, kk.y, kk.z, kk.w};
+      for (int k = 0; k < KB; ++k) s[i][k] = 0.f;
+#pragma unroll 4
+    for (int c4 = 0; c4 < D; c4 += 4) {
+      float4 qv[RT], kv[KB];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) qv[i] = *reinterpret_cast<const float4*>(sQ + (ty + 16 * i) * TS + c4);
+#pragma unroll
+      for (int k = 0; k < KB; ++k) kv[k] = *reinterpret_cast<const float4*>(sK + (tx + 16 * k) * TS + c4);
 #pragma unroll
       for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) s[i][k] = fmaf(av[i], kv[k], s[i][k]);
+        for (int k = 0; k < KB; ++k) {
+          s[i][k] = fmaf(qv[i].x, kv[k].x, s[i][k]);
+          s[i][k] = fmaf(qv[i].y, kv[k].y, s[i][k]);
+          s[i][k] = fmaf(qv[i].z, kv[k].z, s[i][k]);
+          s[i][k] = fmaf(qv[i].w, kv[k].w, s[i][k]);
+        }
     }
-    double su[RT][4];
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) su[i][k] = 0.0;
-    for (int c = D; c < DK; ++c) {
-      float av[RT];
-      qrow(c, av);
-      const float4 kk = *reinterpret_cast<const float4*>(sK + c * BN + 4 * tx);
-      const double kv[4] = {kk.x, kk.y, kk.z, kk.w};
-#pragma unroll
-      for (int i = 0; i < RT; ++i)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) su[i][k] = fma(static_cast<double>(av[i]), kv[k], su[i][k]);
+    __syncthreads();  // every thread is done with sK(j)
+    if (more) {
+      load_k(kblk + 1);
+      cp_async_commit();
     }
+    const double* kf = sKf + (kblk & 1) * R * BN;
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
-      const int row = q0 + RT * ty + i;
-      double sd[4];
+      const int rl = ty + 16 * i, row = q0 + rl;
+      double su[KB];  // the factor term of row i, fp64
+#pragma unroll
+      for (int k = 0; k < KB; ++k) su[k] = 0.0;
+      for (int c = 0; c < R; ++c) {
+        const double a = sQf[c * BM + rl];
+#pragma unroll
+        for (int k = 0; k < KB; ++k) su[k] = fma(a, kf[c * BN + tx + 16 * k], su[k]);
+      }
+      double sd[KB];
       double mx = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int j = kv0 + 4 * tx + k;
-        double v = (static_cast<double>(s[i][k]) + su[i][k]) * static_cast<double>(p.scale);
-        if (p.bias && j < p.M && row < p.N)
+      for (int k = 0; k < KB; ++k) {
+        const int j = kv0 + tx + 16 * k;
+        double v = (static_cast<double>(s[i][k]) + su[k]) * static_cast<double>(p.scale);
+        if (p.bias && (!edge || (j < p.M && row < p.N)))
           v += p.bias[b * p.bias_sb + h * p.bias_sh + static_cast<int64_t>(row) * p.bias_sn + j];
-        if (j >= p.M || (p.causal && j > row)) v = -INFINITY;
+        if (edge && (j >= p.M || (p.causal && j > row))) v = -INFINITY;
         sd[k] = v;
         mx = fmax(mx, v);
       }
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       const double m_new = fmax(m_run[i], mx);
-      float pk[4] = {0.f, 0.f, 0.f, 0.f};
+      float pk[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) pk[k] = 0.f;
       float alpha = 1.f;
       if (m_new != -INFINITY) {
         alpha = expf(static_cast<float>(m_run[i] - m_new));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) pk[k] = expf(static_cast<float>(sd[k] - m_new));
+        for (int k = 0; k < KB; ++k) pk[k] = expf(static_cast<float>(sd[k] - m_new));
         m_run[i] = m_new;
       }
       float ps = (pk[0] + pk[1]) + (pk[2] + pk[3]);
@@ -686,31 +717,47 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
       l_run[i] = l_run[i] * alpha + ps;
 #pragma unroll
       for (int c = 0; c < CPT; ++c) acc[i][c] *= alpha;
-      *reinterpret_cast<float4*>(sP + (RT * ty + i) * PST + 4 * tx) = make_float4(pk[0], pk[1], pk[2], pk[3]);
+#pragma unroll
+      for (int k = 0; k < KB; ++k) sP[rl * PST + tx + 16 * k] = pk[k];
+    }
+    if (more) load_kf(kblk + 1);  // the other buffer: its previous readers finished before the last barrier
+    cp_async_wait<1>();  // V(j) landed (K(j+1) may still be in flight)
+    __syncthreads();
+#pragma unroll 2
+    for (int j4 = 0; j4 < BN; j4 += 4) {
+      float4 pv4[RT];
+#pragma unroll
+      for (int i = 0; i < RT; ++i) pv4[i] = *reinterpret_cast<const float4*>(sP + (ty + 16 * i) * PST + j4);
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        float vv[CPT];
+        if constexpr (CPT >= 4) {
+#pragma unroll
+          for (int c4 = 0; c4 < CPT; c4 += 4) {
+            const float4 w = *reinterpret_cast<const float4*>(sV + (j4 + jj) * D + CPT * tx + c4);
+            vv[c4] = w.x; vv[c4 + 1] = w.y; vv[c4 + 2] = w.z; vv[c4 + 3] = w.w;
+          }
+        } else {
+          const float2 w = *reinterpret_cast<const float2*>(sV + (j4 + jj) * D + CPT * tx);
+          vv[0] = w.x; vv[1] = w.y;
+        }
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const float pv = jj == 0 ? pv4[i].x : jj == 1 ? pv4[i].y : jj == 2 ? pv4[i].z : pv4[i].w;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) acc[i][c] = fmaf(pv, vv[c], acc[i][c]);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with sV(j) and sP
+    if (more) {
+      load_v(kblk + 1);
+      cp_async_commit();
+      cp_async_wait<1>();  // K(j+1) landed (V(j+1) may still be in flight)
     }
     __syncthreads();
-#pragma unroll 4
-    for (int j = 0; j < BN; ++j) {
-      float pv[RT];
-#pragma unroll
-      for (int i = 0; i < RT; ++i) pv[i] = sP[(RT * ty + i) * PST + j];
-      float vv[CPT];
-      if constexpr (CPT >= 4) {
-#pragma unroll
-        for (int c4 = 0; c4 < CPT; c4 += 4) {
-          const float4 w = *reinterpret_cast<const float4*>(sV + j * D + CPT * tx + c4);
-          vv[c4] = w.x; vv[c4 + 1] = w.y; vv[c4 + 2] = w.z; vv[c4 + 3] = w.w;
-        }
-      } else {
-        const float2 w = *reinterpret_cast<const float2*>(sV + j * D + CPT * tx);
-        vv[0] = w.x; vv[1] = w.y;
-      }
-#pragma unroll
-      for (int i = 0; i < RT; ++i)
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) acc[i][c] = fmaf(pv[i], vv[c], acc[i][c]);
-    }
   }
+  cp_async_wait<0>();
   if constexpr (SPLIT > 1) {
     // partials -> this CTA's smem (the K/V region is free): per row m (double), l, then acc[D]
     __syncthreads();
@@ -719,7 +766,7 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
     float* pa = pl + BM;                                   // [BM][D]
 #pragma unroll
     for (int i = 0; i < RT; ++i) {
-      const int r = RT * ty + i;
+      const int r = ty + 16 * i;
       if (tx == 0) {
         pm[r] = m_run[i];
         pl[r] = l_run[i];
@@ -728,56 +775,54 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
       for (int c = 0; c < CPT; ++c) pa[r * D + CPT * tx + c] = acc[i][c];
     }
     cluster_sync_all();  // every rank's partial is written (release / acquire at cluster scope)
-    if (rank == 0) {
-      const uint32_t base = smem_u32(sK);
+    // rank k combines rows [k*BM/SPLIT, (k+1)*BM/SPLIT): one float4 of head columns per thread per step
+    constexpr int RS = BM / SPLIT;
+    const uint32_t base = smem_u32(sK);
+    for (int idx = t; idx < RS * C4; idx += 256) {
+      const int r = rank * RS + idx / C4, c4 = (idx % C4) * 4, row = q0 + r;
+      double mr[SPLIT];
+      float lr[SPLIT];
+      double m_all = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const int r = RT * ty + i;
-        double m_all = -INFINITY;
-        double mr[SPLIT];
-        float lr[SPLIT];
+      for (int k = 0; k < SPLIT; ++k) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(k));
+        asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(mr[k]) : "r"(ra + 8u * r));
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lr[k]) : "r"(ra + 8u * BM + 4u * r));
+        m_all = fmax(m_all, mr[k]);
+      }
+      float wsum = 0.f;
+      float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int k = 0; k < SPLIT; ++k) {
-          uint32_t ra;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(k));
-          asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(mr[k]) : "r"(ra + 8u * r));
-          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lr[k]) : "r"(ra + 8u * BM + 4u * r));
-          m_all = fmax(m_all, mr[k]);
-        }
-        float wsum = 0.f, w[SPLIT];
-#pragma unroll
-        for (int k = 0; k < SPLIT; ++k) {
-          w[k] = mr[k] == -INFINITY ? 0.f : expf(static_cast<float>(mr[k] - m_all));
-          wsum += w[k] * lr[k];
-        }
-        float o[CPT];
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) o[c] = 0.f;
-#pragma unroll
-        for (int k = 0; k < SPLIT; ++k) {
-          uint32_t ra;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(k));
-#pragma unroll
-          for (int c = 0; c < CPT; ++c) {
-            float x;
-            asm volatile("ld.shared::cluster.f32 %0, [%1];"
-                         : "=f"(x)
-                         : "r"(ra + 12u * BM + 4u * (r * D + CPT * tx + c)));
-            o[c] = fmaf(w[k], x, o[c]);
-          }
-        }
-        m_run[i] = m_all;
-        l_run[i] = wsum;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) acc[i][c] = o[c];
+      for (int k = 0; k < SPLIT; ++k) {
+        const float w = mr[k] == -INFINITY ? 0.f : expf(static_cast<float>(mr[k] - m_all));
+        wsum += w * lr[k];
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(base), "r"(k));
+        float4 x;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                     : "r"(ra + 12u * BM + 4u * (r * D + c4)));
+        o.x = fmaf(w, x.x, o.x);
+        o.y = fmaf(w, x.y, o.y);
+        o.z = fmaf(w, x.z, o.z);
+        o.w = fmaf(w, x.w, o.w);
+      }
+      if (row < p.N) {
+        const float inv = wsum > 0.f ? 1.0f / wsum : 0.f;
+        *reinterpret_cast<float4*>(p.o + b * p.o_sb + h * p.o_sh + static_cast<int64_t>(row) * p.o_sn + c4) =
+            make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+        if (p.lse && c4 == 0)
+          p.lse[(static_cast<int64_t>(b) * p.H + h) * p.N + row] =
+              static_cast<float>(m_all + log(static_cast<double>(wsum)));
       }
     }
-    cluster_sync_all();  // peers stay resident until rank 0 has read their partials
-    if (rank != 0) return;
+    cluster_sync_all();  // peers stay resident until every rank has read their partials
+    return;
   }
 #pragma unroll
   for (int i = 0; i < RT; ++i) {
-    const int row = q0 + RT * ty + i;
+    const int row = q0 + ty + 16 * i;
     if (row >= p.N) continue;
     const float inv = l_run[i] > 0.f ? 1.0f / l_run[i] : 0.f;
 #pragma unroll
@@ -789,11 +834,16 @@ __global__ void __launch_bounds__(256) fwd_simt_tiled_kernel(const SimtParams p)
   }
 }
 
+// Q, K [rows][D + 4], V [64][D], P [BM][72] fp32, then the factor columns fp64: [R][BM] + [2][R][64]
+static size_t simt_tiled_smem(int D, int BM, int R) {
+  return sizeof(float) * (static_cast<size_t>(D + 4) * (BM + 64) + 64 * D + BM * 72) +
+         sizeof(double) * static_cast<size_t>(R) * (BM + 128);
+}
+
 template <int D, int BM, int SPLIT>
 static cudaError_t launch_simt_tiled_bm(const SimtParams& p, cudaStream_t s) {
-  const int DK = D + p.R;
   // the split-KV partials (m double, l, acc: 12 + 4D bytes per row) reuse the K/V region
-  const size_t smem = sizeof(float) * (static_cast<size_t>(DK) * (BM + 64) + 64 * D + BM * 68);
+  const size_t smem = simt_tiled_smem(D, BM, p.R);
   static std::atomic<uint64_t> attr_mask{0};
   auto kern = fwd_simt_tiled_kernel<D, BM, SPLIT>;
   cudaError_t e = smem_attr_once(attr_mask, reinterpret_cast<const void*>(kern), 200 * 1024);
@@ -816,8 +866,8 @@ static cudaError_t launch_simt_tiled_bm(const SimtParams& p, cudaStream_t s) {
 
 template <int D>
 static cudaError_t launch_simt_tiled(const SimtParams& p, cudaStream_t s) {
-  // fill ~4 CTAs per SM: 64-row blocks, and a split-KV cluster of 2 / 4 / 8 CTAs per row block
-  // when there are too few row blocks (each CTA keeps >= 2 KV blocks of 64 keys)
+  // ~3-4 CTAs per SM (d <= 64: 80 registers, ~72 KB smem): 64-row blocks, and a split-KV cluster of 2 / 4 / 8
+  // CTAs per row block when there are too few row blocks (each CTA keeps >= 2 KV blocks of 64 keys)
   const int64_t rowblocks = static_cast<int64_t>((p.N + 63) / 64) * p.H * p.B;
   const int kvb = (p.M + 63) / 64;
   if (rowblocks * 8 <= 4 * 148 && kvb >= 16) return launch_simt_tiled_bm<D, 64, 8>(p, s);
@@ -832,9 +882,10 @@ cudaError_t launch_fwd_simt_f32(const SimtParams& p, cudaStream_t s) {
   auto al16 = [](const float* ptr, int64_t sn) {
     return (reinterpret_cast<uintptr_t>(ptr) % 16) == 0 && sn % 4 == 0;
   };
-  const bool aligned = al16(p.q, p.q_sn) && al16(p.k, p.k_sn) && al16(p.v, p.v_sn) && p.q_sb % 4 == 0 &&
-                       p.q_sh % 4 == 0 && p.k_sb % 4 == 0 && p.k_sh % 4 == 0 && p.v_sb % 4 == 0 && p.v_sh % 4 == 0;
-  if (aligned && DK <= 256 && (p.D == 32 || p.D == 64 || p.D == 128)) {
+  const bool aligned = al16(p.q, p.q_sn) && al16(p.k, p.k_sn) && al16(p.v, p.v_sn) && al16(p.o, p.o_sn) &&
+                       p.q_sb % 4 == 0 && p.q_sh % 4 == 0 && p.k_sb % 4 == 0 && p.k_sh % 4 == 0 &&
+                       p.v_sb % 4 == 0 && p.v_sh % 4 == 0 && p.o_sb % 4 == 0 && p.o_sh % 4 == 0;
+  if (aligned && (p.D == 32 || p.D == 64 || p.D == 128) && simt_tiled_smem(p.D, 64, p.R) <= 200 * 1024) {
     cudaError_t e = p.D == 32 ? launch_simt_tiled<32>(p, s)
                     : p.D == 64 ? launch_simt_tiled<64>(p, s) : launch_simt_tiled<128>(p, s);
     note_launch();
