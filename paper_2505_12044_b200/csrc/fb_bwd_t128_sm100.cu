@@ -104,7 +104,7 @@ struct T128Cfg {
   static constexpr int kQ0 = kRes;
   static constexpr int kDO = kQ0 + 2 * kQSlot;
   static constexpr int kDS = kDO + kTile;
-  static constexpr int kStage = kDS + kTile;   // 2 x 8 KB fp32: 16 queries x 128 dims (transposed, SW64)
+  static constexpr int kStage = kDS + kTile;   // 2 x 8 KB fp32: 16 queries x 128 dims (dUq chunk: SW64 rows)
   static constexpr int kStats = kStage + 32 * 128 * 4;
   static constexpr int kBars = kStats + 2 * 2 * 128 * 4;
   static constexpr int kSmem = 1024 + kBars + 256;
@@ -483,11 +483,11 @@ __global__ void __launch_bounds__(512, 1)
   } else {
     regs_inc<T128_REG_DR>();
     // -------------------------------------------------------------- dQ drain (warps 8-11)
-    // dQ^T (lane = head dim) goes to a TRANSPOSED fp32 accumulator [B,H,D,N]
-    // (queries contiguous), so each thread's row of the 16-query stage is 64
-    // contiguous bytes: 4 x st.shared.v4 in the 64-byte swizzle the reduce-add
-    // tensor map uses (conflict-free).  Two 8 KB stages, one reduction in flight
-    // while the next chunk is written.
+    // dQ^T (lane = head dim) is reduce-added into the fp32 accumulator [B,H,N,128]
+    // (head dims contiguous) in 16-query x 128-dim boxes: thread dd writes column
+    // dd of each query row of the stage (a warp writes 128 contiguous bytes per
+    // query: conflict-free), so each box row the L2 reduces is a full 512-byte
+    // line.  Two 8 KB stages, one reduction in flight while the next is written.
     const int dd = threadIdx.x - 256;  // head-dim index = TMEM lane of dQ^T
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
     const bool leader = dd == 0;
@@ -544,26 +544,22 @@ __global__ void __launch_bounds__(512, 1)
       if (lane == 0) mbar_arrive(&bars->dq_free);
 #pragma unroll
       for (int c = 0; c < (skip ? 0 : 128 / QC); ++c, ++chunk) {
-        uint8_t* stg = reinterpret_cast<uint8_t*>(dq_stage) + (chunk % NST) * (128 * RB);
+        // stage = [16 queries][128 dims] fp32: thread dd writes column dd (consecutive words per query row)
+        float* stg = dq_stage + (chunk % NST) * (QC * 128);
         if (leader) trace(p.trace, p.trace_cta, 26, j * 8 + c);
         if (leader) t128_wait_read<NST - 1>();  // the reduction that last read this stage has finished reading
         if (leader) trace(p.trace, p.trace_cta, 27, j * 8 + c);
         named_bar_sync(3, 128);
         const float sc = p.scale;
 #pragma unroll
-        for (int c4 = 0; c4 < QC / 4; ++c4) {
-          const int e = QC * c + 4 * c4;
-          *reinterpret_cast<float4*>(stg + dd * RB + ((c4 ^ ((dd * RB >> 7) & (RB / 16 - 1))) << 4)) =
-              make_float4(__uint_as_float(v[e]) * sc, __uint_as_float(v[e + 1]) * sc, __uint_as_float(v[e + 2]) * sc,
-                          __uint_as_float(v[e + 3]) * sc);
-        }
+        for (int qq = 0; qq < QC; ++qq) stg[qq * 128 + dd] = __uint_as_float(v[QC * c + qq]) * sc;
         if (leader) trace(p.trace, p.trace_cta, 28, j * 8 + c);
         fence_proxy_async();
         if (leader) trace(p.trace, p.trace_cta, 29, j * 8 + c);
         named_bar_sync(3, 128);
         if (leader) {
           trace(p.trace, p.trace_cta, 30, j * 8 + c);
-          t128_reduce_add(&tm_dqacc, stg, q0 + QC * c, 0, h, b);
+          t128_reduce_add(&tm_dqacc, stg, 0, q0 + QC * c, h, b);
           t128_bulk_commit();
         }
       }
@@ -629,55 +625,6 @@ static cudaError_t launch_t128_t(const BwdMaps& m, const CUtensorMap& dqacc, con
   if (T128_MULTICAST && nkt % 2 == 0) return launch_t128_mc<RP, BF16, true, LEARN>(m, dqacc, duq, p, s);
   return launch_t128_mc<RP, BF16, false, LEARN>(m, dqacc, duq, p, s);
 }
-
-// dq[b,h,n,:] = acc_t[b,h,:,n]: 64-query x 128-dim tiles transposed through
-// shared memory; float4 loads along queries, 16-byte bf16 stores along the head dim.
-template <bool BF16>
-__global__ void __launch_bounds__(256) dq_convert_t_kernel(const float* __restrict__ acc, void* dq, int H, int N,
-                                                           int n4, int64_t sb, int64_t sh, int64_t sn, int plane0) {
-  typedef typename std::conditional<BF16, __nv_bfloat16, __half>::type elem_t;
-  __shared__ float tile[64][129];  // [query][dim], odd stride
-  const int bh = plane0 + blockIdx.y, q0 = blockIdx.x * 64;
-  const int bb = bh / H, hh = bh % H;
-  const float* src = acc + static_cast<int64_t>(bh) * 128 * n4;
-  const int t = threadIdx.x;
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {  // 128 dims x 16 float4 (64 queries)
-    const int i = it * 256 + t, d = i >> 4, q4 = (i & 15) * 4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (q0 + q4 + 3 < n4) v = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(d) * n4 + q0 + q4);
-    tile[q4][d] = v.x;
-    tile[q4 + 1][d] = v.y;
-    tile[q4 + 2][d] = v.z;
-    tile[q4 + 3][d] = v.w;
-  }
-  __syncthreads();
-  elem_t* dst = reinterpret_cast<elem_t*>(dq) + static_cast<int64_t>(bb) * sb + static_cast<int64_t>(hh) * sh;
-#pragma unroll
-  for (int it = 0; it < 4; ++it) {  // 64 queries x 16 chunks of 8 dims
-    const int i = it * 256 + t, qq = i >> 4, d8 = (i & 15) * 8;
-    if (q0 + qq < N) {
-      const float* r = &tile[qq][d8];
-      *reinterpret_cast<uint4*>(dst + static_cast<int64_t>(q0 + qq) * sn + d8) =
-          make_uint4(pack2<BF16>(r[0], r[1]), pack2<BF16>(r[2], r[3]), pack2<BF16>(r[4], r[5]), pack2<BF16>(r[6], r[7]));
-    }
-  }
-}
-
-cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, bool bf16, cudaStream_t s) {
-  const int planes = p.B * p.H;
-  for (int plane0 = 0; plane0 < planes; plane0 += 65535) {  // grid.y limit
-    dim3 grid((p.N + 63) / 64, planes - plane0 < 65535 ? planes - plane0 : 65535);
-    if (bf16)
-      dq_convert_t_kernel<true><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn, plane0);
-    else
-      dq_convert_t_kernel<false><<<grid, 256, 0, s>>>(acc_t, p.dq, p.H, p.N, n4, p.dq_sb, p.dq_sh, p.dq_sn, plane0);
-  }
-  return cudaGetLastError();
-}
-
-int bwd_t128_qchunk() { return T128_QCHUNK; }
-int bwd_t128_box_rows() { return 128; }
 
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads) {
   return d == 128 && !dense && (factor_grads ? rp == 1 : rp <= 1);

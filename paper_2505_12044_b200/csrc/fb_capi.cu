@@ -452,19 +452,11 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
     CUtensorMap macc;
     if ((rc = make_map(&macc, &tacc, D, 32, 0, "dq_acc"))) return rc;
     if (use_t128) {
-      // transposed accumulator [B,H,D,N4]: qchunk-query x 128-dim boxes, swizzled to the row width
-      const int64_t n4 = ((int64_t)N + 3) / 4 * 4;
-      fb_tensor tt{};
-      tt.data = acc;
-      tt.shape[0] = B; tt.shape[1] = H; tt.shape[2] = D; tt.shape[3] = N;
-      tt.stride[3] = 1; tt.stride[2] = n4; tt.stride[1] = n4 * D; tt.stride[0] = n4 * D * H;
-      tt.dtype = FB_F32;
-      CUtensorMap macc_t;
-      if ((rc = make_map(&macc_t, &tt, bwd_t128_qchunk(), bwd_t128_box_rows(), bwd_t128_qchunk() * 4, "dq_acc_t"))) return rc;
-      e = cudaMemsetAsync(acc, 0, (size_t)B * H * n4 * D * sizeof(float), s);
+      // the [B,H,N,128] accumulator in 16-query x 128-dim boxes (full 512-byte rows, no swizzle)
+      CUtensorMap macc16;
+      if ((rc = make_map(&macc16, &tacc, D, 16, 0, "dq_acc16"))) return rc;
+      e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * D * sizeof(float), s);
       if (e != cudaSuccess) return cuda_fail(e, "memset dq_acc");
-      p.dq_acc = acc;
-      p.acc_n4 = (int)n4;
       CUtensorMap mduq;
       memset(&mduq, 0, sizeof(mduq));
       if (duq) {  // dUq is reduce-added in 128-query x 16-column boxes: start from zero
@@ -479,11 +471,11 @@ int fb_attn_bwd_ex(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, c
             if (e != cudaSuccess) return cuda_fail(e, "memset duq");
           }
       }
-      e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, duq != nullptr, maps, macc_t, mduq, p, s);
+      e = launch_bwd_t128_sm100(rp, q->dtype == FB_BF16, duq != nullptr, maps, macc16, mduq, p, s);
       if (e != cudaSuccess) return cuda_fail(e, "bwd_t128_sm100");
-      e = launch_dq_convert_t(acc, (int)n4, p, q->dtype == FB_BF16, s);
+      e = launch_dq_convert(acc, D, p, q->dtype == FB_BF16, s);
       note_launch(2);
-      return e == cudaSuccess ? FB_OK : cuda_fail(e, "dq_convert_t");
+      return e == cudaSuccess ? FB_OK : cuda_fail(e, "dq_convert");
     }
     // the 64-query kernels reduce into the untransposed [B,H,N,D] accumulator: start from zero
     e = cudaMemsetAsync(acc, 0, (size_t)B * H * N * D * sizeof(float), s);

@@ -58,7 +58,6 @@ struct BwdParams {
   float* duq; int64_t duq_sb, duq_sh, duq_sn;  // nullable, fp32 [B,H,N,Rpad]
   float* duk; int64_t duk_sb, duk_sh, duk_sn;
   int uq_bb, uq_hb, uk_bb, uk_hb, bias_bb, bias_hb;
-  float* dq_acc; int acc_n4;  // 128x128-tile kernel: transposed fp32 dQ accumulator [B,H,128,acc_n4]
   void* dbias; int64_t db_sb, db_sh, db_sn;  // nullable: learnable dense bias gradient [B,H,N,M] (bias dtype)
   unsigned long long* trace; int trace_cta;  // FB_TRACE builds only
 };
@@ -107,14 +106,11 @@ cudaError_t launch_bwd_fused_sm100(int rp, bool dense, bool bf16, const BwdMaps&
 // d = 128 on 128-key x 128-query tiles (every GEMM N = 128), Rpad <= 16 (factor gradients: Rpad == 16), no
 // dense bias
 bool bwd_t128_supported(int d, int rp, bool dense, bool factor_grads);
-int bwd_t128_qchunk();
-int bwd_t128_box_rows();  // head-dim rows per dQ reduce box (128, or 32 for per-warp boxes)  // queries per dQ reduce box (transposed accumulator map: box {qchunk, 128}, swizzle qchunk*4 B)
 // fgrad: dUq reduce-added through `duq` (fp32 [B,H,N,16], box {16, 128}, 64-byte swizzle, zeroed by the
 // caller), dUk written to p.duk
 cudaError_t launch_bwd_t128_sm100(int rp, bool bf16, bool fgrad, const BwdMaps& maps, const CUtensorMap& dqacc,
                                   const CUtensorMap& duq, const BwdParams& p, cudaStream_t s);
 // dq[b,h,n,:] = acc_t[b,h,:,n] (transposed fp32 accumulator [B,H,128,n4] of the 128x128-tile kernel)
-cudaError_t launch_dq_convert_t(const float* acc_t, int n4, const BwdParams& p, bool bf16, cudaStream_t s);
 cudaError_t launch_dq_convert(const float* acc, int d, const BwdParams& p, bool bf16, cudaStream_t s);
 // single-pass backward for d = 64 (optionally with factor gradients, Rpad <= 64)
 cudaError_t launch_bwd_fused64_sm100(int rp, bool dense, bool bf16, bool fgrad, const BwdMaps& maps,
