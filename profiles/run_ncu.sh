@@ -14,8 +14,11 @@ ARGS="--config $CFG --steps 1 --warmup 1 --skip-dense --skip-e2e --skip-cpu --sk
 export BENCH_PROFILE_RANGE=1
 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${TAG}_${CFG}.csv python bench.py $ARGS > gpurun_out/launches_${TAG}_${CFG}.log 2>&1
-for K in fb_fwd_kernel "fb_bwd_(t128|fused|fused64|dkv)_kernel"; do
-  NAME=$( [ "$K" = fb_fwd_kernel ] && echo fwd || echo bwd )
+KS='fb_fwd_kernel "fb_bwd_(t128|fused|fused64|dkv)_kernel"'
+[ "$CFG" = C1 ] && KS=fwd_simt_tiled_kernel  # the fp32 SIMT forward is the whole C1 step
+eval "set -- $KS"
+for K in "$@"; do
+  NAME=$( [ "$K" = "fb_bwd_(t128|fused|fused64|dkv)_kernel" ] && echo bwd || echo fwd )
   ncu --profile-from-start off --set full --clock-control none --import-source on -k "regex:${K}" -s 1 -c 1 \
       -o gpurun_out/prof_${TAG}_${CFG}_${NAME} -f python bench.py $ARGS > /dev/null 2>&1 || true
   # gpurun copies back <= 64 MiB: keep the raw-page CSV (what summarize.py reads), drop the report unless asked

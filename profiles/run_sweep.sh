@@ -13,6 +13,7 @@ run() {  # name, bench args...
   timeout 900 python bench.py "$@" > gpurun_out/bench_${TAG}_${name}.json 2> gpurun_out/bench_${TAG}_${name}.err
   echo "$name rc=$? $(head -c 300 gpurun_out/bench_${TAG}_${name}.json)"
 }
+run C3 --config C3
 run C1 --config C1 --steps 20 --warmup 5
 run C2 --config C2 --steps 20 --warmup 5
 run C2s --config C2 --steps 20 --warmup 5 --static-factors
@@ -25,5 +26,5 @@ run C3L --config C3 --steps 5 --warmup 3 --learnable --skip-e2e --skip-sdpa
 run MIX --config MIX --steps 20 --warmup 5
 run ref --impl reference --steps 2 --warmup 0
 if [ "$NCU" = ncu ]; then
-  for CFG in C2 C4 C5; do timeout 900 bash profiles/run_ncu.sh "$TAG" "$CFG"; done
+  for CFG in C3 C2 C4 C5 C1; do timeout 900 bash profiles/run_ncu.sh "$TAG" "$CFG"; done
 fi
