@@ -721,7 +721,8 @@ __global__ void __launch_bounds__(256, D <= 64 ? 3 : 1) fwd_simt_tiled_kernel(co
       for (int k = 0; k < KB; ++k) sP[rl * PST + tx + 16 * k] = pk[k];
     }
     if (more) load_kf(kblk + 1);  // the other buffer: its previous readers finished before the last barrier
-    cp_async_wait<1>();  // V(j) landed (K(j+1) may still be in flight)
+    if (more) cp_async_wait<1>();  // V(j) landed (K(j+1) may still be in flight)
+    else cp_async_wait<0>();
     __syncthreads();
 #pragma unroll 2
     for (int j4 = 0; j4 < BN; j4 += 4) {
