@@ -547,7 +547,8 @@ def run_gpu(args, cfg):
                     "frac": round(tflops / fp32_peak, 4),
                     "peak_kind": "nominal fp32 FFMA peak (148 SMs x 128 lanes x 2 x 1965 MHz); no measured fp32 peak",
                     "traffic": None}
-    e2e = run_e2e(cfg, inp, args, device, dist=dist, total_bh=total_bh) if not args.skip_e2e else None
+    e2e = run_e2e(cfg, inp, args, device, chunks=args.e2e_chunks, dist=dist, total_bh=total_bh) \
+        if not args.skip_e2e else None
     result = {
         "metric": METRIC, "value": round(tflops, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True,
@@ -965,6 +966,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="never CUDA-graph the step (small configs use graphs)")
     ap.add_argument("--learnable", action="store_true",
                     help="C4/C5: learnable bias on both arms (FlashBias dfq/dfk vs dense dB); C2 is learnable by default")
+    ap.add_argument("--e2e-chunks", type=int, default=32,
+                    help="head slices the e2e step is software-pipelined over (H2D / compute / D2H)")
     ap.add_argument("--static-factors", action="store_true",
                     help="C2: treat the spatial bias as fixed on both arms (no factor / bias gradients)")
     args = ap.parse_args()
