@@ -310,10 +310,9 @@ size_t fb_bwd_workspace_bytes(const fb_tensor* q, const fb_tensor* k) {
   if (!q) return 0;
   const size_t rows = (size_t)q->shape[0] * q->shape[1] * q->shape[2];
   size_t bytes = (rows * sizeof(float) + 255) / 256 * 256 + 256;  // delta
-  // fp32 dQ accumulator: [B,H,N,D] or, for the 128x128-tile kernel, [B,H,D,N4] (N4 = N rounded up to 4)
-  const size_t n4 = ((size_t)q->shape[2] + 3) / 4 * 4;
+  // fp32 dQ accumulator of the fused backwards: [B,H,N,D]
   if (q->shape[3] == 128 || q->shape[3] == 64)
-    bytes += (size_t)q->shape[0] * q->shape[1] * n4 * q->shape[3] * sizeof(float);
+    bytes += (size_t)q->shape[0] * q->shape[1] * q->shape[2] * q->shape[3] * sizeof(float);
   return bytes;
 }
 

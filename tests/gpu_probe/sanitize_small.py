@@ -39,7 +39,11 @@ for D, causal, kind in cases:
     torch.autograd.grad(o, wrt, do)
     torch.cuda.synchronize()
     print("ok", D, mask, kind, flush=True)
-qf, kf, vf = (torch.randn(1, 2, 200, 64, device="cuda") for _ in range(3))
-fb.flashbias_attention(qf, kf, vf, torch.randn(1, 2, 200, 2, device="cuda"), torch.randn(1, 2, 200, 2, device="cuda"))
-torch.cuda.synchronize()
+# fp32 SIMT forward: split-KV clusters of 2 (N=200) and 4 (N=1024, the C1 shape), causal and ragged
+for n, causal in ((200, False), (1024, False), (333, True)):
+    qf, kf, vf = (torch.randn(1, 2, n, 64, device="cuda") for _ in range(3))
+    fb.flashbias_attention(qf, kf, vf, torch.randn(1, 2, n, 2, device="cuda"), torch.randn(1, 2, n, 2, device="cuda"),
+                           mask="causal" if causal else "none")
+    torch.cuda.synchronize()
+    print("ok fp32", n, causal, flush=True)
 print("SANITIZE_WORKLOAD_DONE")
