@@ -39,12 +39,14 @@ bwd = grab()
 names = {2: "MMA S", 3: "MMA PV", 4: "load", 5: "sm start", 6: "sm end(w0)", 10: "mma dV", 11: "mma ST(c+1)",
          12: "mma dK", 13: "mma dQT", 14: "mma dPT(c+1)", 15: "A start", 16: "A end(w0)", 17: "B start",
          18: "B end(w0)", 19: "drain start", 20: "drain end", 21: "load"}
+import json as _json
+_json.dump({"fwd": fwd, "bwd": bwd}, open(os.environ.get("TRACE_DUMP", "gpurun_out/trace_events.json"), "w"))
 for nm, tl in (("fwd", fwd), ("bwd", bwd)):
     print(f"===== {nm}: {len(tl)} events, span {tl[-1][0]} cycles")
     for t, e, a in tl[: 90 if nm == "fwd" else 120]:
         if 22 <= e <= 29:
             continue
-        print(f"{t:9d} {names.get(e, e):13s} {a}")
+        print(f"{t:9d} {str(names.get(e, e)):13s} {a}")
 d = collections.defaultdict(dict)
 for t, e, a in fwd:
     d[a][e] = t
