@@ -753,7 +753,7 @@ def run_e2e(cfg, inp, args, device, chunks: int = 8, dist=None, total_bh=None):
                     outs[n][bb:bb + 1, a:b].copy_(res[n][bb:bb + 1, a:b], non_blocking=True)
         comp.wait_stream(s_out)  # the step ends when the last D2H lands
 
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 5))
     ms = time_steps(step, steps, 1, dist)
     world = 1
     if dist is not None:  # whole job: every rank moves its own heads over its own PCIe link; max over ranks
