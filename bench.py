@@ -527,7 +527,13 @@ def run_gpu(args, cfg):
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+        e = 2  # bf16 operands: the bwd reads q, k, v, dO and writes dq, dk, dv; the fwd reads q, k, v, writes o
+        alg_bytes = (7 if dom == "bwd" else 4) * n_loc * cfg["N"] * cfg["d"] * e
         roofline = {
+            "traffic_algorithmic": alg_bytes,
+            "traffic_note": ("ncu dram__bytes_read+write of one launch (profiles/ncu_traffic.json); the bwd excess over "
+                             "the algorithmic bytes is the fp32 dQ accumulator's zero-fill read and write-back"
+                             if dom == "bwd" else "ncu dram__bytes_read+write of one launch"),
             "bound": "tensor", "kernel": "fb_attn_bwd (dKV+dQ)" if dom == "bwd" else "fb_attn_fwd (K1)",
             "achieved": round(achieved, 1), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
             "frac": round(achieved / pk["bf16_tflops"], 4), "peak_kind": pk_kind,
