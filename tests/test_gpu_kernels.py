@@ -109,6 +109,25 @@ def test_fwd_fp32_simt(causal):
     assert relerr(out, ref) < F32_TOL
 
 
+@pytest.mark.parametrize("D", [32, 64, 128])
+@pytest.mark.parametrize("N,M,causal", [(64, 64, False), (65, 130, False), (128, 128, True), (200, 200, False),
+                                        (333, 333, True), (1000, 1000, False), (700, 2100, False)])
+def test_fwd_fp32_simt_split_kv_shapes(D, N, M, causal):
+    """The fp32 SIMT forward over the shapes that pick each split-KV cluster size (1/2/4/8 CTAs per row
+    block) with one or several KV blocks per CTA, ragged tails, causal diagonals, factors and a dense
+    bias; parity 1e-5 against torch float64."""
+    H = 4
+    q, k, v = _qkv(1, H, N, M, D, torch.float32, seed=N + M + D)
+    fq = torch.randn(1, H, N, 2, device="cuda") * 0.5
+    fk = torch.randn(1, H, M, 2, device="cuda") * 0.5
+    mask = "causal" if causal else "none"
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask=mask)
+    assert relerr(out, ref_attention(q, k, v, fq, fk, causal=causal)) < F32_TOL
+    bias = torch.randn(1, H, N, M, device="cuda")
+    out = fb.tiled_attention(q, k, v, fb.DenseBias(bias), mask=mask)
+    assert relerr(out, ref_attention(q, k, v, bias=bias, causal=causal)) < F32_TOL
+
+
 def _bwd_case(B, H, N, M, D, R, causal, dense=False, seed=0):
     q, k, v = _qkv(B, H, N, M, D, torch.bfloat16, seed=seed)
     q.requires_grad_(True)
