@@ -527,6 +527,8 @@ def run_gpu(args, cfg):
         tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+            if traffic is not None and n_loc != total_bh:  # captured at N=1: this rank's share of the heads
+                traffic = traffic * n_loc / total_bh
         e = 2  # bf16 operands: the bwd reads q, k, v, dO and writes dq, dk, dv; the fwd reads q, k, v, writes o
         alg_bytes = (7 if dom == "bwd" else 4) * n_loc * cfg["N"] * cfg["d"] * e
         roofline = {
