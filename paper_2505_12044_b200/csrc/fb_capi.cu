@@ -229,6 +229,9 @@ int fb_attn_fwd(const fb_tensor* q, const fb_tensor* k, const fb_tensor* v, cons
     if ((uq && (uq->dtype != FB_F32 || uk->dtype != FB_F32)) || (bias && bias->dtype != FB_F32))
       return fail(FB_EVALUE, "fp32 path needs fp32 factors and bias");
     Tensor4 tq = to_t4(q), tk = to_t4(k), tv = to_t4(v), to = to_t4(o);
+    if (B > 65535 || H > 65535)
+      return fail(FB_ECONFIG, "fp32 path: at most 65535 batch rows and 65535 heads per call (got %lld x %lld); "
+                              "pass head slices", (long long)B, (long long)H);
     SimtParams p{};
     p.B = B; p.H = H; p.N = N; p.M = M; p.D = D; p.R = R;
     p.causal = mask == FB_MASK_CAUSAL;

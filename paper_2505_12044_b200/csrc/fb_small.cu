@@ -67,27 +67,29 @@ __global__ void prepare_factors_kernel(Tensor4 f, int side, int split, float pre
   const int np = (split * (split + 1)) / 2;
   const int L = static_cast<int>(out.shape[2]), Hh = static_cast<int>(out.shape[1]);
   const int rpad = static_cast<int>(out.shape[3]);
-  const int plane = blockIdx.y;
-  const int64_t b = plane / Hh, h = plane % Hh;
+  const int64_t planes = out.shape[0] * out.shape[1];
   const float mul = side == 0 ? premul : 1.0f;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < L * rpad; idx += gridDim.x * blockDim.x) {
-    const int c = idx % rpad, l = idx / rpad;
-    float v = 0.f;
-    if (c < R * np) {
-      const int r = c / np;
-      int a, bpart;
-      pair_parts(c % np, a, bpart);
-      const float x = load_elem(f.data, off4(f, b, h, l, r), f.dtype) * mul;
-      v = split_part(x, side == 0 ? a : bpart, out.dtype);
+  for (int64_t plane = blockIdx.y; plane < planes; plane += gridDim.y) {  // grid.y <= 65535
+    const int64_t b = plane / Hh, h = plane % Hh;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < L * rpad; idx += gridDim.x * blockDim.x) {
+      const int c = idx % rpad, l = idx / rpad;
+      float v = 0.f;
+      if (c < R * np) {
+        const int r = c / np;
+        int a, bpart;
+        pair_parts(c % np, a, bpart);
+        const float x = load_elem(f.data, off4(f, b, h, l, r), f.dtype) * mul;
+        v = split_part(x, side == 0 ? a : bpart, out.dtype);
+      }
+      store_elem(out.data, off4(out, b, h, l, c), out.dtype, v);
     }
-    store_elem(out.data, off4(out, b, h, l, c), out.dtype, v);
   }
 }
 
 // Fast path: one thread per 8-column chunk of a panel row, one 16-byte store.
 template <bool BF16>
 __device__ __forceinline__ void prepare_rows_plane(const Tensor4& f, int side, int split, float premul,
-                                                   const Tensor4& out, int plane) {
+                                                   const Tensor4& out, int64_t plane) {
   const int R = static_cast<int>(f.shape[3]);
   const int np = (split * (split + 1)) / 2;
   const int L = static_cast<int>(out.shape[2]), Hh = static_cast<int>(out.shape[1]);
@@ -122,7 +124,8 @@ __device__ __forceinline__ void prepare_rows_plane(const Tensor4& f, int side, i
 template <bool BF16>
 __global__ void __launch_bounds__(256) prepare_factors_rows_kernel(Tensor4 f, int side, int split, float premul,
                                                                    Tensor4 out) {
-  prepare_rows_plane<BF16>(f, side, split, premul, out, blockIdx.y);
+  for (int64_t plane = blockIdx.y; plane < out.shape[0] * out.shape[1]; plane += gridDim.y)
+    prepare_rows_plane<BF16>(f, side, split, premul, out, plane);
 }
 
 // both panels in one launch: blockIdx.z = side (0: uq from fq with premul, 1: uk from fk)
@@ -132,8 +135,8 @@ __global__ void __launch_bounds__(256) prepare_factor_pair_kernel(Tensor4 fq, Te
   const int side = blockIdx.z;
   const Tensor4& f = side == 0 ? fq : fk;
   const Tensor4& out = side == 0 ? uq : uk;
-  if (blockIdx.y >= out.shape[0] * out.shape[1]) return;
-  prepare_rows_plane<BF16>(f, side, split, premul, out, blockIdx.y);
+  for (int64_t plane = blockIdx.y; plane < out.shape[0] * out.shape[1]; plane += gridDim.y)
+    prepare_rows_plane<BF16>(f, side, split, premul, out, plane);
 }
 
 cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float premul, const Tensor4& out,
@@ -155,11 +158,10 @@ cudaError_t launch_prepare_factor_pair(const Tensor4& fq, const Tensor4& fk, int
   const int64_t planes = pq > pk ? pq : pk;
   const int64_t rows = uq.shape[2] > uk.shape[2] ? uq.shape[2] : uk.shape[2];
   if (planes <= 0 || rows <= 0) return cudaSuccess;
-  if (planes > 65535) return cudaErrorInvalidValue;
   int64_t gx = (rows * (uq.shape[3] / 8) + 255) / 256;
   const int64_t cap = (148 * 16 + planes - 1) / planes;
   if (gx > cap) gx = cap < 1 ? 1 : cap;
-  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(planes), 2);
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(planes < 65535 ? planes : 65535), 2);
   if (uq.dtype == 1) prepare_factor_pair_kernel<true><<<grid, 256, 0, s>>>(fq, fk, split, premul, uq, uk);
   else prepare_factor_pair_kernel<false><<<grid, 256, 0, s>>>(fq, fk, split, premul, uq, uk);
   note_launch();
@@ -171,19 +173,20 @@ cudaError_t launch_prepare_factors(const Tensor4& f, int side, int split, float 
   const int64_t per_plane = out.shape[2] * out.shape[3];
   const int64_t planes = out.shape[0] * out.shape[1];
   if (per_plane <= 0 || planes <= 0) return cudaSuccess;
-  if (planes > 65535 || per_plane > (int64_t(1) << 30)) return cudaErrorInvalidValue;
+  if (per_plane > (int64_t(1) << 30)) return cudaErrorInvalidValue;
+  const unsigned gy = static_cast<unsigned>(planes < 65535 ? planes : 65535);  // kernels stride over planes
   if (rows_ok(out)) {
     int64_t gx = (out.shape[2] * (out.shape[3] / 8) + 255) / 256;
     const int64_t cap = (148 * 16 + planes - 1) / planes;
     if (gx > cap) gx = cap < 1 ? 1 : cap;
-    dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(planes));
+    dim3 grid(static_cast<unsigned>(gx), gy);
     if (out.dtype == 1) prepare_factors_rows_kernel<true><<<grid, 256, 0, s>>>(f, side, split, premul, out);
     else prepare_factors_rows_kernel<false><<<grid, 256, 0, s>>>(f, side, split, premul, out);
   } else {
     int64_t gx = (per_plane + 255) / 256;
     const int64_t cap = (148 * 16 + planes - 1) / planes;
     if (gx > cap) gx = cap < 1 ? 1 : cap;
-    prepare_factors_kernel<<<dim3(static_cast<unsigned>(gx), static_cast<unsigned>(planes)), 256, 0, s>>>(
+    prepare_factors_kernel<<<dim3(static_cast<unsigned>(gx), gy), 256, 0, s>>>(
         f, side, split, premul, out);
   }
   note_launch();
@@ -353,12 +356,13 @@ __global__ void bwd_preprocess_kernel(Tensor4 o, Tensor4 dout, Tensor4 delta) {
 // group; grid.y = the (b, h) plane.  HBM-bound: reads O and dO once.
 template <typename T, int TPR>
 __global__ void __launch_bounds__(256) bwd_preprocess_vec_kernel(const T* __restrict__ o, const T* __restrict__ dout,
-                                                                 float* __restrict__ delta, int H, int N,
+                                                                 float* __restrict__ delta, int H, int N, int64_t planes,
                                                                  int64_t o_sb, int64_t o_sh, int64_t o_sn,
                                                                  int64_t d_sb, int64_t d_sh, int64_t d_sn) {
   constexpr int RPB = 256 / TPR;
-  const int plane = blockIdx.y, b = plane / H, h = plane % H;
   const int sub = threadIdx.x % TPR;
+  for (int64_t plane = blockIdx.y; plane < planes; plane += gridDim.y) {  // grid.y <= 65535
+  const int64_t b = plane / H, h = plane % H;
   const T* ob = o + b * o_sb + h * o_sh + sub * 8;
   const T* db = dout + b * d_sb + h * d_sh + sub * 8;
   for (int i = blockIdx.x * RPB + threadIdx.x / TPR; i < N; i += gridDim.x * RPB) {
@@ -375,7 +379,8 @@ __global__ void __launch_bounds__(256) bwd_preprocess_vec_kernel(const T* __rest
     float sum = acc.x + acc.y;
 #pragma unroll
     for (int m = TPR / 2; m > 0; m >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
-    if (sub == 0) delta[static_cast<int64_t>(plane) * N + i] = sum;
+    if (sub == 0) delta[plane * N + i] = sum;
+  }
   }
 }
 
@@ -388,13 +393,14 @@ static void launch_pre_vec(const Tensor4& o, const Tensor4& dout, const Tensor4&
   int64_t gx = (N + rpb - 1) / rpb;
   const int64_t cap = (148 * 8 + B * H - 1) / (B * H);
   if (gx > cap) gx = cap < 1 ? 1 : cap;
-  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(B * H));
+  const int64_t planes = static_cast<int64_t>(B) * H;
+  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(planes < 65535 ? planes : 65535));
   const T* op = reinterpret_cast<const T*>(o.data);
   const T* dp = reinterpret_cast<const T*>(dout.data);
   float* dl = reinterpret_cast<float*>(delta.data);
 #define FB_PRE(TPRV)                                                                                        \
-  bwd_preprocess_vec_kernel<T, TPRV><<<grid, 256, 0, s>>>(op, dp, dl, H, N, o.stride[0], o.stride[1], o.stride[2], \
-                                                          dout.stride[0], dout.stride[1], dout.stride[2])
+  bwd_preprocess_vec_kernel<T, TPRV><<<grid, 256, 0, s>>>(op, dp, dl, H, N, planes, o.stride[0], o.stride[1],   \
+                                                          o.stride[2], dout.stride[0], dout.stride[1], dout.stride[2])
   if (tpr == 16) FB_PRE(16);
   else if (tpr == 8) FB_PRE(8);
   else FB_PRE(4);

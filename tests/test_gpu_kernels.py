@@ -31,7 +31,8 @@ def ref_attention(q, k, v, fq=None, fk=None, bias=None, causal=False, scale=None
 
 
 def relerr(a, b):
-    return float((a.double() - b.double()).abs().max() / b.double().abs().max().clamp_min(1e-30))
+    a, b = a.detach().double(), b.detach().double()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
 
 
 def _qkv(B, H, N, M, D, dtype, seed=0):
@@ -126,6 +127,27 @@ def test_fwd_fp32_simt_split_kv_shapes(D, N, M, causal):
     bias = torch.randn(1, H, N, M, device="cuda")
     out = fb.tiled_attention(q, k, v, fb.DenseBias(bias), mask=mask)
     assert relerr(out, ref_attention(q, k, v, bias=bias, causal=causal)) < F32_TOL
+
+
+def test_many_heads_over_grid_y_limit():
+    """B*H = 70000 planes (> the 65535 grid.y limit of the plane-indexed helper kernels: factor-panel
+    split, backward preprocess): forward + backward with factors against torch float64 on sampled heads."""
+    B, H, N, D = 2, 35000, 16, 64
+    q, k, v = _qkv(B, H, N, N, D, torch.bfloat16, seed=5)
+    for t in (q, k, v):
+        t.requires_grad_(True)
+    fq = torch.randn(B, H, N, 2, device="cuda") * 0.5
+    fk = torch.randn(B, H, N, 2, device="cuda") * 0.5
+    do = torch.randn(B, H, N, D, device="cuda").bfloat16()
+    out = fb.flashbias_attention(q, k, v, fq, fk, mask="causal")
+    out.backward(do)
+    for b, h in ((0, 0), (1, 34999), (1, 30000)):
+        qs, ks, vs = (t.detach()[b:b + 1, h:h + 1].double().requires_grad_(True) for t in (q, k, v))
+        ref = ref_attention(qs, ks, vs, fq[b:b + 1, h:h + 1], fk[b:b + 1, h:h + 1], causal=True)
+        assert relerr(out[b:b + 1, h:h + 1], ref) < BF16_TOL
+        ref.backward(do[b:b + 1, h:h + 1].double())
+        for got, t in ((q.grad, qs), (k.grad, ks), (v.grad, vs)):
+            assert relerr(got[b:b + 1, h:h + 1], t.grad) < BF16_TOL
 
 
 def _bwd_case(B, H, N, M, D, R, causal, dense=False, seed=0):
