@@ -85,6 +85,27 @@ def test_bf16_path_matches_oracle_on_rounded_inputs(case):
     assert orc.rel_max_err(got, _oracle(case, r)) <= BF16_TOL
 
 
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_reference_attention_matches_reference_golden(case):
+    """reference_attention / attention_weights (ref attention.py:111-137: the materialised float64
+    formula the reference's own tests use as ground truth) against the reference's golden outputs of
+    every instance (dense, factored -- FactoredBias.dense() = fq fk^T, unscaled -- and no bias)."""
+    lib = fb()
+    a = _inputs(case)
+    if "bias" in a:
+        bias = lib.DenseBias(a["bias"])
+    elif "fq" in a:
+        bias = lib.FactoredBias(a["fq"], a["fk"])
+    else:
+        bias = lib.NO_BIAS
+    got = lib.reference_attention(a["q"], a["k"], a["v"], bias, mask=case["mask"])
+    assert isinstance(got, np.ndarray) and got.dtype == np.float64
+    assert orc.rel_max_err(got, G[f"{case['name']}/o"]) <= 1e-10
+    w = lib.attention_weights(a["q"], a["k"], bias, mask=case["mask"])
+    assert np.allclose(w.sum(axis=-1), 1.0, atol=1e-12)
+    assert orc.rel_max_err(w @ np.asarray(a["v"], dtype=np.float64), G[f"{case['name']}/o"]) <= 1e-10
+
+
 def test_criterion1_all_200_instances_both_paths():
     """Acceptance criterion 1 (reference test_acceptance.py:27-48): 200 seeded
     instances, random shapes/masks/ranks.  fp32 path vs the reference's
